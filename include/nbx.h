@@ -1,0 +1,220 @@
+/*
+ * nbx.h -- C-ABI of the B200-native NBNXM cluster-pair nonbonded engine (libnbx.so).
+ *
+ * The reference (arxiv/paper_2405_01420 = the `mdgpusim` step-schedule simulator) has no
+ * physics API: its whole representation of this hot path is the cost law
+ *     CostTable.duration_ns(kind, atoms, backend, scale)      pkg/src/mdgpusim/costs.py:137-140
+ * priced per KernelKind (costs.py:28-43) and submitted per MD step by pipeline.simulate
+ * (pipeline.py:222-261 single rank, 321-431 domain-decomposed).  Each entry point below is
+ * the real computation behind one of those simulated kernels; the replaced reference
+ * interface is cited on each declaration.  DESIGN.md pins the physics, the cluster
+ * geometry and the list format that the reference leaves unspecified.
+ *
+ * Conventions
+ *  - Plain C types only.  "dev" pointers are CUDA device pointers on the context's device,
+ *    "host" pointers are host memory.  Streams are cudaStream_t passed as void*.
+ *  - Every function returns an nbx_status; on failure nbx_last_error() returns a
+ *    thread-local message.  No C++ exception crosses the ABI.
+ *  - One context = one device; calls on one context are stream-ordered and NOT thread-safe.
+ *  - There is no CPU fallback: without a usable sm_100 device nbx_create fails with
+ *    NBX_ECUDA.
+ *
+ * Units: nm, ps, e, kJ/mol.  Coordinates/forces are float32 [n][3].
+ */
+#ifndef NBX_H
+#define NBX_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NBX_API __attribute__((visibility("default")))
+
+/* ---- status codes ---------------------------------------------------------------------- */
+typedef enum {
+    NBX_OK = 0,
+    NBX_EINVAL = 1,         /* bad argument / call order                                   */
+    NBX_ECUDA = 2,          /* CUDA runtime error or no sm_100 device                      */
+    NBX_ENOMEM = 3,         /* device allocation failed                                    */
+    NBX_ELIST_OVERFLOW = 4, /* list or mask pool larger than the 24-bit pool index allows  */
+    NBX_ENCCL = 5           /* reserved for the halo layer                                 */
+} nbx_status;
+
+/* ---- parameters (mirrors the reference's per-system knobs, presets.py:28-49) ------------ */
+enum { NBX_COULOMB_RF = 0, NBX_COULOMB_EWALD = 1 };
+
+typedef struct nbx_params {
+    int32_t coulomb_type; /* NBX_COULOMB_RF or NBX_COULOMB_EWALD                           */
+    float rc;             /* common LJ/Coulomb cut-off (presets.py:40 cutoff_nm)           */
+    float rlist_outer;    /* pair-search radius, list lifetime nstlist (presets.py:44)     */
+    float rlist_inner;    /* dynamic-prune radius, lifetime prune_every (presets.py:45)    */
+    float epsilon_r;      /* relative dielectric constant                                  */
+    float epsilon_rf;     /* reaction-field dielectric; 0 means infinity                   */
+    float ewald_rtol;     /* erfc(beta*rc) = ewald_rtol                                    */
+} nbx_params;
+
+/* Derived constants, computed identically (double, then rounded once) by the library and
+ * by the CPU oracle; exported so tests can check them.                                    */
+typedef struct nbx_consts {
+    float epsfac;   /* 138.935458 / epsilon_r                                            */
+    float k_rf;     /* RF: (eps_rf-eps_r)/((2eps_rf+eps_r) rc^3), or 1/(2rc^3) if eps_rf=inf */
+    float c_rf;     /* RF: 1/rc + k_rf rc^2                                               */
+    float beta;     /* Ewald splitting coefficient (1/nm)                                 */
+    float sh_ewald; /* erfc(beta rc)/rc                                                   */
+    float sh_lj6;   /* rc^-6                                                              */
+    float sh_lj12;  /* rc^-12                                                             */
+    float rc2;      /* rc^2                                                               */
+    float rlo2;     /* rlist_outer^2                                                      */
+    float rli2;     /* rlist_inner^2                                                      */
+} nbx_consts;
+
+/* ---- pair-list format ----------------------------------------
+ * Cluster geometry: i-cluster = 4 atoms, j-cluster = 8 atoms = i-clusters {2cj, 2cj+1},
+ * super-cluster (sci) = 32 atoms = i-clusters 8sci..8sci+7 = j-clusters 4sci..4sci+3.
+ * A list is: sci entries (sci, shift, [cj_start, cj_end)), cj entries (cj, imask | pool<<8)
+ * and a mask pool; pool[0] is implicit "all pairs interact, no exclusion correction".   */
+typedef struct nbx_sci_entry {
+    int32_t sci;
+    int32_t shift;    /* 0..26 = (sz+1)*9 + (sy+1)*3 + (sx+1); 13 is the central image */
+    int32_t cj_start;
+    int32_t cj_end;
+} nbx_sci_entry;
+
+typedef struct nbx_cj_entry {
+    int32_t cj;
+    uint32_t meta; /* bits 0-7: i-cluster interaction mask, bits 8-31: mask-pool index    */
+} nbx_cj_entry;
+
+/* pool element p: 8 i-clusters x {interaction mask, exclusion-correction mask}, each a
+ * 32-bit word with bit (i*8 + j) for i-atom i (0..3) and j-atom j (0..7).                */
+typedef struct nbx_mask_pool_entry {
+    uint32_t m[8][2];
+} nbx_mask_pool_entry;
+
+enum { NBX_NSHIFT = 27, NBX_CENTRAL_SHIFT = 13 };
+enum { NBX_LIST_LOCAL = 0, NBX_LIST_NONLOCAL = 1 };
+enum { NBX_GRID_LOCAL = 0, NBX_GRID_NONLOCAL = 1 };
+
+/* force flags */
+enum {
+    NBX_FORCE_ENERGY = 1u << 0, /* accumulate E_lj, E_coul (fp64)                         */
+    NBX_FORCE_VIRIAL = 1u << 1  /* accumulate shift forces for the virial                 */
+};
+
+typedef struct nbx_ctx nbx_ctx;
+
+/* ---- lifecycle ------------------------------------------------------------------------- */
+NBX_API const char* nbx_last_error(void);
+NBX_API const char* nbx_version(void);
+
+/* Derive the constants of a parameter set (no device needed).                           */
+NBX_API int nbx_derive_consts(const nbx_params* p, nbx_consts* out);
+
+/* Create a context on `device` (must be sm_100).  Replaces the reference's per-rank device
+ * construction (_RankBuild -> Device/RankRuntime, runtime.py:255-304).                   */
+NBX_API int nbx_create(int device, const nbx_params* p, nbx_ctx** out);
+NBX_API int nbx_destroy(nbx_ctx* ctx);
+
+/* Topology over the GLOBAL atom set (host arrays; uploaded once).
+ * q[n], type[n] in [0,ntypes), c6c12[ntypes*ntypes*2] = plain (c6, c12) with
+ * V = c12/r^12 - c6/r^6, exclusions CSR over global ids (symmetric, self not listed).
+ * Replaces the per-system sizes of SystemPreset (presets.py:28-60).                      */
+NBX_API int nbx_set_topology(nbx_ctx* ctx, int32_t natoms_global, const float* q_host,
+                             const int32_t* type_host, int32_t ntypes,
+                             const float* c6c12_host, const int32_t* excl_offsets_host,
+                             const int32_t* excl_gids_host);
+
+/* Rectangular box edges (nm) and per-dimension periodicity of the searched images
+ * (0 for dimensions split by domain decomposition, whose images arrive as halo atoms).    */
+NBX_API int nbx_set_box(nbx_ctx* ctx, const float box_host[3], const int32_t pbc_host[3]);
+
+/* ---- grid + pair search: KernelKind.PAIR_SEARCH (costs.py:32,163; pipeline.py:226-230)
+ * Build grid `grid` from n atoms: x_dev[n][3] (user order), gid_dev[n] global ids
+ * (NULL = identity, single domain).  Region [lo, lo+size) in nm (single domain: 0, box). */
+NBX_API int nbx_grid_build(nbx_ctx* ctx, int grid, int32_t n, const float* x_dev,
+                           const int32_t* gid_dev, const float lo_host[3],
+                           const float size_host[3], void* stream);
+
+/* Build list `list` (LOCAL: grid0 x grid0 half list; NONLOCAL: grid0 i x grid1 j with the
+ * global-id rule) at rlist_outer, then prune it to rlist_inner.  Synchronises `stream`
+ * once to size the list (count pass -> exact allocation -> fill pass).                   */
+NBX_API int nbx_search(nbx_ctx* ctx, int list, void* stream);
+
+/* ---- X buffer op (folded into NBNXM_* in the reference model, pipeline.py:231) ------- *
+ * Copy user-order coordinates of grid `grid` into the cluster-ordered xyzq buffer, with
+ * the wrap shifts fixed at the last grid build.                                          */
+NBX_API int nbx_put_x(nbx_ctx* ctx, int grid, const float* x_dev, void* stream);
+
+/* ---- rolling dynamic prune: KernelKind.PRUNE_ONLY (costs.py:31,162; pipeline.py:233-235)
+ * Re-derive the inner list of `list` from its outer list with the current coordinates,
+ * processing sci entries e with e % nparts == part (nparts=1: whole list).               */
+NBX_API int nbx_prune(nbx_ctx* ctx, int list, int part, int nparts, void* stream);
+
+/* ---- force: KernelKind.NBNXM_LOCAL / NBNXM_NONLOCAL (costs.py:29-30; pipeline.py:231,384)
+ * Accumulate forces of the inner list `list` into the cluster force buffers (and, with
+ * flags, energies / shift forces into the context's fp64 accumulators).                  */
+NBX_API int nbx_force(nbx_ctx* ctx, int list, uint32_t flags, void* stream);
+
+/* ---- F buffer op: KernelKind.REDUCE_FORCES (costs.py:41,172; pipeline.py:250-254,398-401)
+ * Write (accumulate != 0: add) grid `grid`'s cluster forces to f_dev[n][3] in the order of
+ * the grid-build input, and clear the cluster buffer for the next step.                  */
+NBX_API int nbx_get_f(nbx_ctx* ctx, int grid, float* f_dev, int accumulate, void* stream);
+
+/* Energies and virial accumulated since the last clear.  Reads grid buffers, so call it
+ * after nbx_force and BEFORE nbx_get_f.  e_host[2] = {E_lj, E_coul incl. self term},
+ * virial_host[9] = -1/2 sum x (x) f - 1/2 sum s (x) fshift (row-major).  Synchronises.    */
+NBX_API int nbx_energies(nbx_ctx* ctx, double* e_host, double* virial_host, void* stream);
+NBX_API int nbx_clear_energies(nbx_ctx* ctx, void* stream);
+
+/* ---- introspection (tests, bench) ------------------------------------------------------ */
+typedef struct nbx_list_sizes {
+    int64_t n_sci;      /* sci entries                                                   */
+    int64_t n_cj_outer; /* cj entries of the outer list                                  */
+    int64_t n_cj_inner; /* cj entries of the inner list (sum of kept)                    */
+    int64_t n_pool;     /* mask-pool entries including the implicit entry 0              */
+} nbx_list_sizes;
+
+typedef struct nbx_grid_info {
+    int32_t n;      /* atoms                                                              */
+    int32_t nslots; /* padded cluster-ordered slots (multiple of 32)                      */
+    int32_t ncx, ncy;
+} nbx_grid_info;
+
+NBX_API int nbx_grid_info_get(nbx_ctx* ctx, int grid, nbx_grid_info* out);
+/* order_host[nslots] (input index or -1), xq_host[nslots*4], type_host[nslots]; any NULL. */
+NBX_API int nbx_grid_export(nbx_ctx* ctx, int grid, int32_t* order_host, float* xq_host,
+                            int32_t* type_host);
+NBX_API int nbx_list_sizes_get(nbx_ctx* ctx, int list, nbx_list_sizes* out);
+/* Copy the list to host.  which = 0 outer, 1 inner (inner cj entries are compacted into
+ * canonical contiguous order, with sci entries' ranges rewritten accordingly).           */
+NBX_API int nbx_list_export(nbx_ctx* ctx, int list, int which, nbx_sci_entry* sci_host,
+                            nbx_cj_entry* cj_host, nbx_mask_pool_entry* pool_host);
+
+/* Count, over the inner list, the interacting atom pairs inside the cut-off (interaction
+ * bit set, r < rc: the "pair-interactions" of the benchmark metric) and the computed pair
+ * slots (32 per active i-cluster x j-cluster tile).  Synchronises `stream`.              */
+NBX_API int nbx_count_pairs(nbx_ctx* ctx, int list, int64_t* pairs_out, int64_t* slots_out,
+                            void* stream);
+
+/* Measured FP32 FFMA peak of this device (TFLOP/s) from a register-resident FMA loop;
+ * used as the roofline denominator.                              */
+NBX_API int nbx_fma_peak(nbx_ctx* ctx, double* tflops_out, void* stream);
+
+/* Number of kernel launches this context has issued (bench evidence: gpu_launches).    */
+NBX_API int64_t nbx_launch_count(nbx_ctx* ctx);
+
+/* ---- domain-decomposition halo (KernelKind.HALO_PACK_UNPACK, costs.py:43,174;
+ *      pipeline.py:363-380 coordinates, 403-418 forces) -------------------------------- *
+ * pack:   out[k] = x[idx[k]] + shift  (k < n)                                              *
+ * unpack_add: f[idx[k]] += in[k]                                                          */
+NBX_API int nbx_halo_pack_x(const float* x_dev, const int32_t* idx_dev, int32_t n,
+                            const float shift_host[3], float* out_dev, void* stream);
+NBX_API int nbx_halo_unpack_add_f(float* f_dev, const int32_t* idx_dev, int32_t n,
+                                  const float* in_dev, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NBX_H */

@@ -1,0 +1,471 @@
+// capi.cu -- the extern "C" boundary of libnbx.so (include/nbx.h).  Every entry point
+// catches all errors and returns an nbx_status with a thread-local message; no exception
+// crosses the ABI.  There is no CPU fallback anywhere in this library.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "nbx_internal.cuh"
+
+namespace nbx {
+
+static thread_local std::string g_err;
+
+void set_error(const std::string& msg) { g_err = msg; }
+
+int fail(int code, const std::string& msg)
+{
+    g_err = msg;
+    return code;
+}
+
+static double ewald_beta(double rc, double rtol)
+{
+    double lo = 0.0, hi = 5.0;
+    while (std::erfc(hi * rc) > rtol) hi *= 2.0;
+    for (int it = 0; it < 60; it++) {
+        double mid = 0.5 * (lo + hi);
+        if (std::erfc(mid * rc) > rtol) lo = mid; else hi = mid;
+    }
+    return 0.5 * (lo + hi);
+}
+
+// identical formulas to ora_derive_consts (oracle/nbx_oracle.c)
+static int derive(const nbx_params* p, nbx_consts* c)
+{
+    const double rc = p->rc;
+    std::memset(c, 0, sizeof(*c));
+    c->epsfac = (float)(138.935458 / (double)p->epsilon_r);
+    double krf;
+    if (p->epsilon_rf == 0.0f)
+        krf = 1.0 / (2.0 * rc * rc * rc);
+    else
+        krf = ((double)p->epsilon_rf - (double)p->epsilon_r) /
+              ((2.0 * (double)p->epsilon_rf + (double)p->epsilon_r) * rc * rc * rc);
+    c->k_rf = (float)krf;
+    c->c_rf = (float)(1.0 / rc + krf * rc * rc);
+    const double beta = (p->coulomb_type == NBX_COULOMB_EWALD) ? ewald_beta(rc, p->ewald_rtol) : 0.0;
+    c->beta = (float)beta;
+    c->sh_ewald = (p->coulomb_type == NBX_COULOMB_EWALD) ? (float)(std::erfc(beta * rc) / rc) : 0.0f;
+    c->sh_lj6 = (float)(1.0 / (rc * rc * rc * rc * rc * rc));
+    c->sh_lj12 = (float)(1.0 / (rc * rc * rc * rc * rc * rc * rc * rc * rc * rc * rc * rc));
+    c->rc2 = (float)(rc * rc);
+    c->rlo2 = (float)((double)p->rlist_outer * (double)p->rlist_outer);
+    c->rli2 = (float)((double)p->rlist_inner * (double)p->rlist_inner);
+    if (!(p->rc > 0.0f) || p->rlist_inner < p->rc || p->rlist_outer < p->rlist_inner) return 1;
+    if (p->coulomb_type != NBX_COULOMB_RF && p->coulomb_type != NBX_COULOMB_EWALD) return 1;
+    if (p->coulomb_type == NBX_COULOMB_EWALD && !(p->ewald_rtol > 0.0f && p->ewald_rtol < 1.0f)) return 1;
+    if (!(p->epsilon_r > 0.0f)) return 1;
+    return 0;
+}
+
+} // namespace nbx
+
+using namespace nbx;
+
+#define NBX_GUARD_BEGIN try {
+#define NBX_GUARD_END                                                                         \
+    }                                                                                         \
+    catch (const CudaError& e)                                                                \
+    {                                                                                         \
+        int code = (e.err == cudaErrorMemoryAllocation) ? NBX_ENOMEM : NBX_ECUDA;            \
+        if (std::strstr(e.what, "24-bit")) code = NBX_ELIST_OVERFLOW;                        \
+        return fail(code, std::string(e.what) + ": " + cudaGetErrorString(e.err));           \
+    }                                                                                         \
+    catch (const std::exception& e)                                                           \
+    {                                                                                         \
+        return fail(NBX_EINVAL, e.what());                                                    \
+    }                                                                                         \
+    catch (...)                                                                               \
+    {                                                                                         \
+        return fail(NBX_EINVAL, "unknown error");                                             \
+    }
+
+#define NBX_CHECK_CTX(ctx)                                                                    \
+    if (!(ctx)) return fail(NBX_EINVAL, "null context");                                      \
+    NBX_CUDA(cudaSetDevice((ctx)->device));
+
+extern "C" {
+
+NBX_API const char* nbx_last_error(void) { return g_err.c_str(); }
+
+NBX_API const char* nbx_version(void) { return "nbx 0.1 (sm_100a)"; }
+
+NBX_API int nbx_derive_consts(const nbx_params* p, nbx_consts* out)
+{
+    if (!p || !out) return fail(NBX_EINVAL, "null argument");
+    if (derive(p, out)) return fail(NBX_EINVAL, "invalid parameters (need 0 < rc <= rlist_inner <= rlist_outer, valid coulomb type)");
+    return NBX_OK;
+}
+
+NBX_API int nbx_create(int device, const nbx_params* p, nbx_ctx** out)
+{
+    NBX_GUARD_BEGIN
+    if (!p || !out) return fail(NBX_EINVAL, "null argument");
+    *out = nullptr;
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev <= device || device < 0)
+        return fail(NBX_ECUDA, std::string("no CUDA device ") + std::to_string(device) + " (" +
+                                   cudaGetErrorString(e) + "); libnbx has no CPU fallback");
+    cudaDeviceProp prop;
+    NBX_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+        return fail(NBX_ECUDA, std::string("device ") + prop.name + " is not sm_100 (built for sm_100a only)");
+    nbx_consts c;
+    if (derive(p, &c)) return fail(NBX_EINVAL, "invalid parameters");
+    NBX_CUDA(cudaSetDevice(device));
+    nbx_ctx* ctx = new nbx_ctx();
+    ctx->device = device;
+    ctx->num_sms = prop.multiProcessorCount;
+    ctx->p = *p;
+    ctx->c = c;
+    ctx->acc.ensure(2 + 3 * NBX_NSHIFT + 9);
+    NBX_CUDA(cudaMemset(ctx->acc.p, 0, sizeof(double) * (2 + 3 * NBX_NSHIFT + 9)));
+    ctx->sumq2.ensure(2);
+    NBX_CUDA(cudaMemset(ctx->sumq2.p, 0, sizeof(double) * 2));
+    ctx->counter.ensure(8);
+    *out = ctx;
+    return NBX_OK;
+    NBX_GUARD_END
+}
+
+NBX_API int nbx_destroy(nbx_ctx* ctx)
+{
+    NBX_GUARD_BEGIN
+    if (!ctx) return NBX_OK;
+    cudaSetDevice(ctx->device);
+    cudaDeviceSynchronize();
+    for (int g = 0; g < 2; g++) {
+        Grid& G = ctx->grid[g];
+        G.col_count.release(); G.col_start.release(); G.col_astart.release();
+        G.key.release(); G.key_out.release(); G.val.release(); G.val_out.release(); G.xw.release();
+        G.order.release(); G.gid.release(); G.type.release(); G.xq.release(); G.wrapk.release();
+        G.f.release(); G.bb_ci.release(); G.bb_cj.release(); G.bb_sci.release();
+        G.exr_ci.release(); G.gr_cj.release(); G.tmp.release();
+        List& L = ctx->list[g];
+        L.sci.release(); L.sci_in.release(); L.cj.release(); L.cj_in.release(); L.pool.release();
+        L.counts.release(); L.offsets.release(); L.totals.release(); L.tmp.release();
+    }
+    ctx->q_g.release(); ctx->type_g.release(); ctx->excl_off_g.release(); ctx->excl_gid_g.release();
+    ctx->c6c12s.release(); ctx->acc.release(); ctx->sumq2.release(); ctx->counter.release();
+    delete ctx;
+    return NBX_OK;
+    NBX_GUARD_END
+}
+
+NBX_API int nbx_set_topology(nbx_ctx* ctx, int32_t n, const float* q, const int32_t* type,
+                             int32_t ntypes, const float* c6c12, const int32_t* excl_offsets,
+                             const int32_t* excl_gids)
+{
+    NBX_GUARD_BEGIN
+    NBX_CHECK_CTX(ctx);
+    if (n < 0 || ntypes <= 0 || !q || !type || !c6c12 || !excl_offsets)
+        return fail(NBX_EINVAL, "bad topology arguments");
+    if ((size_t)ntypes * ntypes * sizeof(float2) > 48 * 1024)
+        return fail(NBX_EINVAL, "too many LJ types for the shared-memory table (max 78)");
+    for (int a = 0; a < n; a++)
+        if (type[a] < 0 || type[a] >= ntypes) return fail(NBX_EINVAL, "atom type out of range");
+    const int nexcl = excl_offsets[n];
+    if (excl_offsets[0] != 0 || nexcl < 0 || (nexcl > 0 && !excl_gids))
+        return fail(NBX_EINVAL, "bad exclusion CSR");
+    for (int e = 0; e < nexcl; e++)
+        if (excl_gids[e] < 0 || excl_gids[e] >= n) return fail(NBX_EINVAL, "exclusion id out of range");
+    ctx->natoms_global = n;
+    ctx->ntypes = ntypes;
+    const int nn = n > 0 ? n : 1;
+    ctx->q_g.ensure(nn);
+    ctx->type_g.ensure(nn);
+    ctx->excl_off_g.ensure(n + 1);
+    ctx->excl_gid_g.ensure(nexcl > 0 ? nexcl : 1);
+    NBX_CUDA(cudaMemcpy(ctx->q_g.p, q, sizeof(float) * n, cudaMemcpyHostToDevice));
+    NBX_CUDA(cudaMemcpy(ctx->type_g.p, type, sizeof(int) * n, cudaMemcpyHostToDevice));
+    NBX_CUDA(cudaMemcpy(ctx->excl_off_g.p, excl_offsets, sizeof(int) * (n + 1), cudaMemcpyHostToDevice));
+    if (nexcl > 0)
+        NBX_CUDA(cudaMemcpy(ctx->excl_gid_g.p, excl_gids, sizeof(int) * nexcl, cudaMemcpyHostToDevice));
+    std::vector<float2> t((size_t)ntypes * ntypes);
+    for (int k = 0; k < ntypes * ntypes; k++)
+        t[k] = make_float2(6.0f * c6c12[2 * k], 12.0f * c6c12[2 * k + 1]);
+    ctx->c6c12s.ensure(t.size());
+    NBX_CUDA(cudaMemcpy(ctx->c6c12s.p, t.data(), sizeof(float2) * t.size(), cudaMemcpyHostToDevice));
+    ctx->have_topology = true;
+    if (ctx->have_box)
+        ctx->density = (double)n / ((double)ctx->box[0] * (double)ctx->box[1] * (double)ctx->box[2]);
+    return NBX_OK;
+    NBX_GUARD_END
+}
+
+NBX_API int nbx_set_box(nbx_ctx* ctx, const float box[3], const int32_t pbc[3])
+{
+    NBX_GUARD_BEGIN
+    NBX_CHECK_CTX(ctx);
+    if (!box) return fail(NBX_EINVAL, "null box");
+    const float rmin = 2.0f * ctx->p.rlist_outer;
+    for (int d = 0; d < 3; d++) {
+        if (!(box[d] > 0.0f)) return fail(NBX_EINVAL, "box edges must be positive");
+        const int per = pbc ? pbc[d] : 1;
+        if (per && box[d] < rmin)
+            return fail(NBX_EINVAL, "periodic box edge shorter than 2 * rlist_outer");
+        ctx->box[d] = box[d];
+        ctx->pbc[d] = per ? 1 : 0;
+    }
+    ctx->have_box = true;
+    if (ctx->have_topology)
+        ctx->density = (double)ctx->natoms_global / ((double)box[0] * (double)box[1] * (double)box[2]);
+    return NBX_OK;
+    NBX_GUARD_END
+}
+
+NBX_API int nbx_grid_build(nbx_ctx* ctx, int grid, int32_t n, const float* x, const int32_t* gid,
+                           const float lo[3], const float size[3], void* stream)
+{
+    NBX_GUARD_BEGIN
+    NBX_CHECK_CTX(ctx);
+    if (grid < 0 || grid > 1) return fail(NBX_EINVAL, "grid must be 0 or 1");
+    if (!ctx->have_topology || !ctx->have_box) return fail(NBX_EINVAL, "set topology and box first");
+    if (n < 0 || (n > 0 && !x) || !lo || !size) return fail(NBX_EINVAL, "bad grid arguments");
+    if (grid == 0 && gid == nullptr && n != ctx->natoms_global)
+        return fail(NBX_EINVAL, "identity gid requires n == natoms_global");
+    for (int d = 0; d < 3; d++)
+        if (!(size[d] > 0.0f)) return fail(NBX_EINVAL, "grid region size must be positive");
+    grid_build(ctx, grid, n, x, gid, lo, size, (cudaStream_t)stream);
+    // a new grid invalidates the lists built on it
+    ctx->list[0].built = ctx->list[0].built && grid != 0;
+    ctx->list[1].built = false;
+    return NBX_OK;
+    NBX_GUARD_END
+}
+
+NBX_API int nbx_search(nbx_ctx* ctx, int list, void* stream)
+{
+    NBX_GUARD_BEGIN
+    NBX_CHECK_CTX(ctx);
+    if (list < 0 || list > 1) return fail(NBX_EINVAL, "list must be 0 or 1");
+    if (!ctx->grid[0].built || (list == 1 && !ctx->grid[1].built))
+        return fail(NBX_EINVAL, "build the grid(s) first");
+    search(ctx, list, (cudaStream_t)stream);
+    return NBX_OK;
+    NBX_GUARD_END
+}
+
+NBX_API int nbx_put_x(nbx_ctx* ctx, int grid, const float* x, void* stream)
+{
+    NBX_GUARD_BEGIN
+    NBX_CHECK_CTX(ctx);
+    if (grid < 0 || grid > 1 || !ctx->grid[grid].built) return fail(NBX_EINVAL, "grid not built");
+    if (!x && ctx->grid[grid].n > 0) return fail(NBX_EINVAL, "null coordinates");
+    put_x(ctx, grid, x, (cudaStream_t)stream);
+    return NBX_OK;
+    NBX_GUARD_END
+}
+
+NBX_API int nbx_prune(nbx_ctx* ctx, int list, int part, int nparts, void* stream)
+{
+    NBX_GUARD_BEGIN
+    NBX_CHECK_CTX(ctx);
+    if (list < 0 || list > 1 || !ctx->list[list].built) return fail(NBX_EINVAL, "list not built");
+    if (nparts < 1 || part < 0 || part >= nparts) return fail(NBX_EINVAL, "bad prune part");
+    prune(ctx, list, part, nparts, (cudaStream_t)stream);
+    return NBX_OK;
+    NBX_GUARD_END
+}
+
+NBX_API int nbx_force(nbx_ctx* ctx, int list, uint32_t flags, void* stream)
+{
+    NBX_GUARD_BEGIN
+    NBX_CHECK_CTX(ctx);
+    if (list < 0 || list > 1 || !ctx->list[list].built) return fail(NBX_EINVAL, "list not built");
+    force(ctx, list, flags, (cudaStream_t)stream);
+    return NBX_OK;
+    NBX_GUARD_END
+}
+
+NBX_API int nbx_get_f(nbx_ctx* ctx, int grid, float* f, int accumulate, void* stream)
+{
+    NBX_GUARD_BEGIN
+    NBX_CHECK_CTX(ctx);
+    if (grid < 0 || grid > 1 || !ctx->grid[grid].built) return fail(NBX_EINVAL, "grid not built");
+    if (!f && ctx->grid[grid].n > 0) return fail(NBX_EINVAL, "null force buffer");
+    get_f(ctx, grid, f, accumulate, (cudaStream_t)stream);
+    return NBX_OK;
+    NBX_GUARD_END
+}
+
+NBX_API int nbx_clear_energies(nbx_ctx* ctx, void* stream)
+{
+    NBX_GUARD_BEGIN
+    NBX_CHECK_CTX(ctx);
+    NBX_CUDA(cudaMemsetAsync(ctx->acc.p, 0, sizeof(double) * (2 + 3 * NBX_NSHIFT + 9), (cudaStream_t)stream));
+    return NBX_OK;
+    NBX_GUARD_END
+}
+
+NBX_API int nbx_energies(nbx_ctx* ctx, double* e, double* vir, void* stream)
+{
+    NBX_GUARD_BEGIN
+    NBX_CHECK_CTX(ctx);
+    cudaStream_t st = (cudaStream_t)stream;
+    const int NA = 2 + 3 * NBX_NSHIFT + 9;
+    NBX_CUDA(cudaMemsetAsync(ctx->acc.p + 2 + 3 * NBX_NSHIFT, 0, sizeof(double) * 9, st));
+    virial_sum(ctx, 0, st);
+    if (ctx->list[1].built) virial_sum(ctx, 1, st);
+    double h[2 + 3 * NBX_NSHIFT + 9];
+    double q2 = 0.0;
+    NBX_CUDA(cudaMemcpyAsync(h, ctx->acc.p, sizeof(double) * NA, cudaMemcpyDeviceToHost, st));
+    NBX_CUDA(cudaMemcpyAsync(&q2, ctx->sumq2.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+    NBX_CUDA(cudaStreamSynchronize(st));
+    double self;
+    if (ctx->p.coulomb_type == NBX_COULOMB_EWALD)
+        self = -(double)ctx->c.epsfac * q2 * (double)ctx->c.beta / std::sqrt(M_PI);
+    else
+        self = -0.5 * (double)ctx->c.epsfac * (double)ctx->c.c_rf * q2;
+    if (e) {
+        e[0] = h[0];
+        e[1] = h[1] + self;
+    }
+    if (vir) {
+        double w[9];
+        for (int k = 0; k < 9; k++) w[k] = h[2 + 3 * NBX_NSHIFT + k];
+        for (int s = 0; s < NBX_NSHIFT; s++) {
+            const int sx = s % 3 - 1, sy = (s / 3) % 3 - 1, sz = s / 9 - 1;
+            const float v[3] = {(float)sx * ctx->box[0], (float)sy * ctx->box[1], (float)sz * ctx->box[2]};
+            for (int a = 0; a < 3; a++)
+                for (int b = 0; b < 3; b++) w[3 * a + b] += (double)v[a] * h[2 + 3 * s + b];
+        }
+        for (int k = 0; k < 9; k++) vir[k] = -0.5 * w[k];
+    }
+    return NBX_OK;
+    NBX_GUARD_END
+}
+
+NBX_API int nbx_grid_info_get(nbx_ctx* ctx, int grid, nbx_grid_info* out)
+{
+    if (!ctx || !out || grid < 0 || grid > 1) return fail(NBX_EINVAL, "bad arguments");
+    const Grid& G = ctx->grid[grid];
+    out->n = G.n;
+    out->nslots = G.nslots;
+    out->ncx = G.ncx;
+    out->ncy = G.ncy;
+    return NBX_OK;
+}
+
+NBX_API int nbx_grid_export(nbx_ctx* ctx, int grid, int32_t* order, float* xq, int32_t* type)
+{
+    NBX_GUARD_BEGIN
+    NBX_CHECK_CTX(ctx);
+    if (grid < 0 || grid > 1 || !ctx->grid[grid].built) return fail(NBX_EINVAL, "grid not built");
+    Grid& G = ctx->grid[grid];
+    NBX_CUDA(cudaDeviceSynchronize());
+    if (order) NBX_CUDA(cudaMemcpy(order, G.order.p, sizeof(int) * G.nslots, cudaMemcpyDeviceToHost));
+    if (xq) NBX_CUDA(cudaMemcpy(xq, G.xq.p, sizeof(float4) * G.nslots, cudaMemcpyDeviceToHost));
+    if (type) NBX_CUDA(cudaMemcpy(type, G.type.p, sizeof(int) * G.nslots, cudaMemcpyDeviceToHost));
+    return NBX_OK;
+    NBX_GUARD_END
+}
+
+NBX_API int nbx_list_sizes_get(nbx_ctx* ctx, int list, nbx_list_sizes* out)
+{
+    NBX_GUARD_BEGIN
+    NBX_CHECK_CTX(ctx);
+    if (list < 0 || list > 1 || !out) return fail(NBX_EINVAL, "bad arguments");
+    List& L = ctx->list[list];
+    out->n_sci = L.built ? L.n_sci : 0;
+    out->n_cj_outer = L.built ? L.n_cj : 0;
+    out->n_pool = L.built ? L.n_pool : 0;
+    out->n_cj_inner = 0;
+    if (L.built && L.n_sci > 0) {
+        NBX_CUDA(cudaDeviceSynchronize());
+        std::vector<nbx_sci_entry> s(L.n_sci);
+        NBX_CUDA(cudaMemcpy(s.data(), L.sci_in.p, sizeof(nbx_sci_entry) * L.n_sci, cudaMemcpyDeviceToHost));
+        int64_t tot = 0;
+        for (auto& e : s) tot += e.cj_end - e.cj_start;
+        out->n_cj_inner = tot;
+    }
+    return NBX_OK;
+    NBX_GUARD_END
+}
+
+NBX_API int nbx_list_export(nbx_ctx* ctx, int list, int which, nbx_sci_entry* sci, nbx_cj_entry* cj,
+                            nbx_mask_pool_entry* pool)
+{
+    NBX_GUARD_BEGIN
+    NBX_CHECK_CTX(ctx);
+    if (list < 0 || list > 1 || !ctx->list[list].built) return fail(NBX_EINVAL, "list not built");
+    List& L = ctx->list[list];
+    NBX_CUDA(cudaDeviceSynchronize());
+    if (pool) NBX_CUDA(cudaMemcpy(pool, L.pool.p, sizeof(nbx_mask_pool_entry) * L.n_pool, cudaMemcpyDeviceToHost));
+    if (which == 0) {
+        if (sci) NBX_CUDA(cudaMemcpy(sci, L.sci.p, sizeof(nbx_sci_entry) * L.n_sci, cudaMemcpyDeviceToHost));
+        if (cj) NBX_CUDA(cudaMemcpy(cj, L.cj.p, sizeof(nbx_cj_entry) * L.n_cj, cudaMemcpyDeviceToHost));
+        return NBX_OK;
+    }
+    std::vector<nbx_sci_entry> s(L.n_sci);
+    std::vector<nbx_cj_entry> c(L.n_cj);
+    if (L.n_sci) NBX_CUDA(cudaMemcpy(s.data(), L.sci_in.p, sizeof(nbx_sci_entry) * L.n_sci, cudaMemcpyDeviceToHost));
+    if (L.n_cj) NBX_CUDA(cudaMemcpy(c.data(), L.cj_in.p, sizeof(nbx_cj_entry) * L.n_cj, cudaMemcpyDeviceToHost));
+    int64_t pos = 0;
+    for (int64_t e = 0; e < L.n_sci; e++) {
+        nbx_sci_entry se = s[e];
+        const int n = se.cj_end - se.cj_start;
+        if (cj && n > 0) std::memcpy(cj + pos, c.data() + se.cj_start, sizeof(nbx_cj_entry) * n);
+        if (sci) {
+            sci[e] = se;
+            sci[e].cj_start = (int32_t)pos;
+            sci[e].cj_end = (int32_t)(pos + n);
+        }
+        pos += n;
+    }
+    return NBX_OK;
+    NBX_GUARD_END
+}
+
+NBX_API int nbx_count_pairs(nbx_ctx* ctx, int list, int64_t* pairs, int64_t* slots, void* stream)
+{
+    NBX_GUARD_BEGIN
+    NBX_CHECK_CTX(ctx);
+    if (list < 0 || list > 1 || !ctx->list[list].built) return fail(NBX_EINVAL, "list not built");
+    long long p = 0, s = 0;
+    count_pairs(ctx, list, &p, &s, (cudaStream_t)stream);
+    if (pairs) *pairs = p;
+    if (slots) *slots = s;
+    return NBX_OK;
+    NBX_GUARD_END
+}
+
+NBX_API int nbx_fma_peak(nbx_ctx* ctx, double* tflops, void* stream)
+{
+    NBX_GUARD_BEGIN
+    NBX_CHECK_CTX(ctx);
+    if (!tflops) return fail(NBX_EINVAL, "null output");
+    *tflops = fma_peak((cudaStream_t)stream);
+    ctx->launches += 4;
+    return NBX_OK;
+    NBX_GUARD_END
+}
+
+NBX_API int64_t nbx_launch_count(nbx_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+NBX_API int nbx_halo_pack_x(const float* x, const int32_t* idx, int32_t n, const float shift[3],
+                            float* out, void* stream)
+{
+    NBX_GUARD_BEGIN
+    if (n < 0 || (n > 0 && (!x || !idx || !out || !shift))) return fail(NBX_EINVAL, "bad halo arguments");
+    if (n == 0) return NBX_OK;
+    halo_pack_x(x, idx, n, make_float3(shift[0], shift[1], shift[2]), out, (cudaStream_t)stream);
+    return NBX_OK;
+    NBX_GUARD_END
+}
+
+NBX_API int nbx_halo_unpack_add_f(float* f, const int32_t* idx, int32_t n, const float* in, void* stream)
+{
+    NBX_GUARD_BEGIN
+    if (n < 0 || (n > 0 && (!f || !idx || !in))) return fail(NBX_EINVAL, "bad halo arguments");
+    halo_unpack_add_f(f, idx, n, in, (cudaStream_t)stream);
+    return NBX_OK;
+    NBX_GUARD_END
+}
+
+} // extern "C"

@@ -1,0 +1,151 @@
+// nbx_internal.cuh -- context, device buffers and shared helpers of libnbx (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/nbx.h"
+
+#define NBX_FILLER_COORD (-1.0e5f)
+#define NBX_BB_EMPTY 1.0e30f
+#define NBX_R2MIN 1.0e-6f
+
+namespace nbx {
+
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+
+struct CudaError {
+    cudaError_t err;
+    const char* what;
+};
+
+#define NBX_CUDA(call)                                                               \
+    do {                                                                             \
+        cudaError_t _e = (call);                                                     \
+        if (_e != cudaSuccess) throw ::nbx::CudaError{_e, #call};                     \
+    } while (0)
+
+// Grow-only device buffer.
+template <class T>
+struct DBuf {
+    T* p = nullptr;
+    size_t cap = 0;
+    void ensure(size_t n)
+    {
+        if (n <= cap && p) return;
+        if (p) NBX_CUDA(cudaFree(p));
+        p = nullptr;
+        size_t want = n < 16 ? 16 : n + n / 8;
+        NBX_CUDA(cudaMalloc((void**)&p, want * sizeof(T)));
+        cap = want;
+    }
+    void release()
+    {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+struct Grid {
+    int n = 0, nslots = 0, nsci = 0, ncx = 0, ncy = 0, ncol = 0;
+    float lo[3] = {0, 0, 0}, size[3] = {0, 0, 0}, inv_cell[2] = {0, 0};
+    bool built = false;
+    DBuf<int> col_count, col_start, col_astart; // [ncol], [ncol+1], [ncol+1]
+    DBuf<unsigned long long> key, key_out;      // sort keys [n]
+    DBuf<int> val, val_out;                     // sort values [n]
+    DBuf<float4> xw;                            // wrapped coords + ... per input atom [n]
+    DBuf<int> order, gid, type;                 // [nslots]
+    DBuf<float4> xq;                            // [nslots] x,y,z,q
+    DBuf<float4> wrapk;                         // [nslots] kx,ky,kz,q
+    DBuf<float4> f;                             // [nslots] cluster forces (w unused)
+    DBuf<float4> bb_ci, bb_cj, bb_sci;          // 2 float4 per cluster: lo (w = nreal), hi
+    DBuf<int2> exr_ci;                          // partner gid range per i-cluster
+    DBuf<int2> gr_cj;                           // gid range per j-cluster
+    DBuf<char> tmp;                             // cub temp
+};
+
+struct List {
+    int64_t n_sci = 0, n_cj = 0, n_pool = 0;
+    bool built = false;
+    int gi = 0, gj = 0, mode = 0;
+    DBuf<nbx_sci_entry> sci, sci_in;
+    DBuf<nbx_cj_entry> cj, cj_in;
+    DBuf<nbx_mask_pool_entry> pool;
+    DBuf<int> counts;  // [3][nsci+1]
+    DBuf<int> offsets; // [3][nsci+1]
+    DBuf<int> totals;  // [3]
+    DBuf<char> tmp;
+};
+
+struct ForceConsts {
+    float epsfac, k_rf, two_k_rf, c_rf, beta, beta2, beta3, sh_ewald, sh_lj6, sh_lj12, rc2, rli2;
+};
+
+} // namespace nbx
+
+struct nbx_ctx {
+    int device = 0;
+    int num_sms = 148;
+    nbx_params p{};
+    nbx_consts c{};
+    int natoms_global = 0, ntypes = 0;
+    bool have_topology = false, have_box = false;
+    float box[3] = {0, 0, 0};
+    int pbc[3] = {1, 1, 1};
+    double density = 0.0;
+    nbx::DBuf<float> q_g;
+    nbx::DBuf<int> type_g;
+    nbx::DBuf<int> excl_off_g, excl_gid_g;
+    nbx::DBuf<float2> c6c12s; // (6 c6, 12 c12)
+    nbx::Grid grid[2];
+    nbx::List list[2];
+    nbx::DBuf<double> acc;    // [0..1] E_lj, E_coul ; [2..82] fshift ; [83..91] sum x (x) f
+    nbx::DBuf<double> sumq2;  // [2] per grid
+    nbx::DBuf<int> counter;   // work counters [8]
+    int64_t launches = 0;
+};
+
+namespace nbx {
+
+// ---- shared device helpers ------------------------------------------------------------
+__device__ __forceinline__ uint32_t ordkey(float f)
+{
+    uint32_t u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+__device__ __forceinline__ void red_add_v4(float4* p, float4 v)
+{
+    asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y),
+                 "f"(v.z), "f"(v.w)
+                 : "memory");
+}
+
+// shift vector of shift index s (0..26): exactly (float)sx * box[d] as in the oracle
+__device__ __forceinline__ float3 shift_vec(int s, float3 box)
+{
+    int sx = s % 3 - 1, sy = (s / 3) % 3 - 1, sz = s / 9 - 1;
+    return make_float3(__fmul_rn((float)sx, box.x), __fmul_rn((float)sy, box.y),
+                       __fmul_rn((float)sz, box.z));
+}
+
+// ---- launchers (defined in the .cu files) -----------------------------------------------
+void grid_build(nbx_ctx* ctx, int g, int n, const float* x, const int* gid, const float lo[3],
+                const float size[3], cudaStream_t st);
+void search(nbx_ctx* ctx, int l, cudaStream_t st);
+void prune(nbx_ctx* ctx, int l, int part, int nparts, cudaStream_t st);
+void count_pairs(nbx_ctx* ctx, int l, long long* pairs, long long* slots, cudaStream_t st);
+void force(nbx_ctx* ctx, int l, unsigned flags, cudaStream_t st);
+void put_x(nbx_ctx* ctx, int g, const float* x, cudaStream_t st);
+void get_f(nbx_ctx* ctx, int g, float* f, int accumulate, cudaStream_t st);
+void virial_sum(nbx_ctx* ctx, int g, cudaStream_t st);
+void halo_pack_x(const float* x, const int* idx, int n, float3 shift, float* out, cudaStream_t st);
+void halo_unpack_add_f(float* f, const int* idx, int n, const float* in, cudaStream_t st);
+double fma_peak(cudaStream_t st);
+ForceConsts make_force_consts(const nbx_consts& c);
+
+} // namespace nbx

@@ -1,0 +1,478 @@
+// search.cu -- cluster-pair search (KernelKind.PAIR_SEARCH, costs.py:32,163; pipeline.py:226-230)
+// and the rolling dynamic prune (KernelKind.PRUNE_ONLY, costs.py:31,162; pipeline.py:233-235).
+//
+// One warp per super-cluster.  Candidate j-clusters of one column are tested 32 per pass
+// (one per lane) against the shifted super-cluster and then the 8 i-cluster bounding boxes
+// at rlist_outer.  The list is written deterministically: a count pass, exclusive scans,
+// then a fill pass that writes every entry at its ballot/popc rank, so the output order is
+// the canonical (sci, shift, cj) order of the CPU oracle (ora_search) bit for bit.
+// The prune tests the 32 atom pairs of every active (i-cluster, j-cluster) tile at
+// rlist_inner with the current coordinates (one pair per lane, any() over the warp).
+#include <cub/device/device_scan.cuh>
+
+#include "nbx_internal.cuh"
+
+namespace nbx {
+
+struct SearchArgs {
+    // i grid
+    const float4* bb_ci;
+    const float4* bb_sci;
+    const int* order_i;
+    const int* gid_i;
+    const int2* exr_ci;
+    int nsci_i;
+    // j grid
+    const float4* bb_cj;
+    const float4* bb_sci_j;
+    const int* order_j;
+    const int* gid_j;
+    const int2* gr_cj;
+    const int* col_start_j;
+    int ncx_j, ncy_j;
+    float lo_jx, lo_jy, inv_jx, inv_jy;
+    // topology
+    const int* excl_off;
+    const int* excl_gid;
+    float3 box;
+    int pbc0, pbc1, pbc2;
+    int mode;
+    float rl, rl2, rlm;
+    // outputs
+    int* counts;        // [3][nsci]
+    const int* offsets; // [3][nsci+1]
+    nbx_sci_entry* sci_out;
+    nbx_cj_entry* cj_out;
+    nbx_mask_pool_entry* pool_out;
+};
+
+__device__ __forceinline__ float bb_dist2(float4 alo, float4 ahi, float3 v, float4 blo, float4 bhi)
+{
+    float ax0 = __fadd_rn(alo.x, v.x), ax1 = __fadd_rn(ahi.x, v.x);
+    float ay0 = __fadd_rn(alo.y, v.y), ay1 = __fadd_rn(ahi.y, v.y);
+    float az0 = __fadd_rn(alo.z, v.z), az1 = __fadd_rn(ahi.z, v.z);
+    float dx = fmaxf(0.0f, fmaxf(__fsub_rn(ax0, bhi.x), __fsub_rn(blo.x, ax1)));
+    float dy = fmaxf(0.0f, fmaxf(__fsub_rn(ay0, bhi.y), __fsub_rn(blo.y, ay1)));
+    float dz = fmaxf(0.0f, fmaxf(__fsub_rn(az0, bhi.z), __fsub_rn(blo.z, az1)));
+    return __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
+}
+
+// interaction / exclusion-correction masks of tile (ci, cj), DESIGN.md "Masks"
+__device__ uint2 tile_masks(const SearchArgs& A, int ci, int cj, bool exov, bool central)
+{
+    uint32_t im = 0u, cm = 0u;
+    for (int i = 0; i < 4; i++) {
+        const int a = 4 * ci + i;
+        if (A.order_i[a] < 0) continue;
+        const int ga = A.gid_i[a];
+        const int e0 = exov ? A.excl_off[ga] : 0, e1 = exov ? A.excl_off[ga + 1] : 0;
+        for (int j = 0; j < 8; j++) {
+            const int b = 8 * cj + j;
+            if (A.order_j[b] < 0) continue;
+            const int gb = A.gid_j[b];
+            const bool present = (A.mode == NBX_LIST_LOCAL) ? !(central && b <= a) : (ga < gb);
+            if (!present) continue;
+            bool ex = false;
+            for (int e = e0; e < e1; e++) ex |= (A.excl_gid[e] == gb);
+            const uint32_t bit = 1u << (i * 8 + j);
+            if (ex) cm |= bit; else im |= bit;
+        }
+    }
+    return make_uint2(im, cm);
+}
+
+// Evaluate one candidate j-cluster; returns imask (bits 0-7) | need_pool (bit 8).
+// With `pool` non-null, also writes the 8 mask pairs of the entry.
+__device__ unsigned eval_candidate(const SearchArgs& A, int sci, int cj, float3 v, bool central,
+                                   float4 slo, float4 shi, nbx_mask_pool_entry* pool)
+{
+    if (A.mode == NBX_LIST_LOCAL && central && cj < 4 * sci) return 0u;
+    const float4 blo = A.bb_cj[2 * cj], bhi = A.bb_cj[2 * cj + 1];
+    if (blo.w == 0.0f) return 0u;
+    if (!(bb_dist2(slo, shi, v, blo, bhi) < A.rl2)) return 0u;
+    const int2 gr = A.gr_cj[cj];
+    unsigned imask = 0u, need = 0u;
+    for (int kk = 0; kk < 8; kk++) {
+        const int ci = 8 * sci + kk;
+        const float4 ilo = A.bb_ci[2 * ci], ihi = A.bb_ci[2 * ci + 1];
+        uint2 m = make_uint2(0u, 0u);
+        if (ilo.w != 0.0f && bb_dist2(ilo, ihi, v, blo, bhi) < A.rl2) {
+            const int2 er = A.exr_ci[ci];
+            const bool exov = !(er.y < gr.x || er.x > gr.y);
+            const bool masked = ilo.w < 4.0f || blo.w < 8.0f || A.mode == NBX_LIST_NONLOCAL ||
+                                (central && (cj >> 2) == sci) || exov;
+            m = make_uint2(0xffffffffu, 0u);
+            if (masked) m = tile_masks(A, ci, cj, exov, central);
+            if ((m.x | m.y) != 0u) {
+                imask |= 1u << kk;
+                if (m.x != 0xffffffffu || m.y != 0u) need = 1u;
+            } else {
+                m = make_uint2(0u, 0u);
+            }
+        }
+        if (pool) {
+            pool->m[kk][0] = m.x;
+            pool->m[kk][1] = m.y;
+        }
+    }
+    return imask | (need << 8);
+}
+
+template <bool FILL>
+__global__ void k_search(SearchArgs A)
+{
+    const int lane = threadIdx.x & 31;
+    const int sci = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (sci >= A.nsci_i) return;
+    const unsigned lt = (1u << lane) - 1u;
+    const float4 slo = A.bb_sci[2 * sci], shi = A.bb_sci[2 * sci + 1];
+    int n_ent = 0, n_cj = 0, n_pool = 0;
+    int ent_base = 0, cj_base = 0, pool_base = 0;
+    if (FILL) {
+        ent_base = A.offsets[sci];
+        cj_base = A.offsets[(A.nsci_i + 1) + sci];
+        pool_base = 1 + A.offsets[2 * (A.nsci_i + 1) + sci];
+    }
+    if (slo.w != 0.0f) {
+        for (int s = 0; s < NBX_NSHIFT; s++) {
+            const int sx = s % 3 - 1, sy = (s / 3) % 3 - 1, sz = s / 9 - 1;
+            if ((!A.pbc0 && sx) || (!A.pbc1 && sy) || (!A.pbc2 && sz)) continue;
+            if (A.mode == NBX_LIST_LOCAL && s < NBX_CENTRAL_SHIFT) continue;
+            const bool central = (s == NBX_CENTRAL_SHIFT);
+            const float3 v = shift_vec(s, A.box);
+            const float lx = __fadd_rn(slo.x, v.x), hx = __fadd_rn(shi.x, v.x);
+            const float ly = __fadd_rn(slo.y, v.y), hy = __fadd_rn(shi.y, v.y);
+            const float lz = __fadd_rn(slo.z, v.z), hz = __fadd_rn(shi.z, v.z);
+            int cx0 = (int)floorf((lx - A.rl - A.lo_jx) * A.inv_jx) - 1;
+            int cx1 = (int)floorf((hx + A.rl - A.lo_jx) * A.inv_jx) + 1;
+            int cy0 = (int)floorf((ly - A.rl - A.lo_jy) * A.inv_jy) - 1;
+            int cy1 = (int)floorf((hy + A.rl - A.lo_jy) * A.inv_jy) + 1;
+            cx0 = max(cx0, 0);
+            cy0 = max(cy0, 0);
+            cx1 = min(cx1, A.ncx_j - 1);
+            cy1 = min(cy1, A.ncy_j - 1);
+            const float zlo = lz - A.rlm, zhi = hz + A.rlm;
+            const int start_cj = n_cj;
+            for (int cx = cx0; cx <= cx1; cx++) {
+                for (int cy = cy0; cy <= cy1; cy++) {
+                    const int col = cx * A.ncy_j + cy;
+                    const int k0 = A.col_start_j[col] >> 5, k1 = A.col_start_j[col + 1] >> 5;
+                    // first slab with hi.z >= zlo, first slab with lo.z > zhi (both monotone)
+                    int a = k0, b = k1;
+                    while (a < b) {
+                        int mid = (a + b) >> 1;
+                        if (A.bb_sci_j[2 * mid + 1].z < zlo) a = mid + 1; else b = mid;
+                    }
+                    const int ks = a;
+                    b = k1;
+                    while (a < b) {
+                        int mid = (a + b) >> 1;
+                        if (A.bb_sci_j[2 * mid].z > zhi) b = mid; else a = mid + 1;
+                    }
+                    const int ke = a;
+                    for (int c0 = 4 * ks; c0 < 4 * ke; c0 += 32) {
+                        const int cj = c0 + lane;
+                        unsigned res = 0u;
+                        if (cj < 4 * ke) res = eval_candidate(A, sci, cj, v, central, slo, shi, nullptr);
+                        const unsigned has = __ballot_sync(0xffffffffu, (res & 0xffu) != 0u);
+                        const unsigned pb = __ballot_sync(0xffffffffu, (res >> 8) != 0u);
+                        if (FILL && (res & 0xffu)) {
+                            unsigned pidx = 0u;
+                            if (res >> 8) {
+                                pidx = (unsigned)(pool_base + n_pool + __popc(pb & lt));
+                                eval_candidate(A, sci, cj, v, central, slo, shi, A.pool_out + pidx);
+                            }
+                            nbx_cj_entry e;
+                            e.cj = cj;
+                            e.meta = (res & 0xffu) | (pidx << 8);
+                            A.cj_out[cj_base + n_cj + __popc(has & lt)] = e;
+                        }
+                        n_cj += __popc(has);
+                        n_pool += __popc(pb);
+                    }
+                }
+            }
+            if (n_cj > start_cj) {
+                if (FILL && lane == 0) {
+                    nbx_sci_entry e;
+                    e.sci = sci;
+                    e.shift = s;
+                    e.cj_start = cj_base + start_cj;
+                    e.cj_end = cj_base + n_cj;
+                    A.sci_out[ent_base + n_ent] = e;
+                }
+                n_ent++;
+            }
+        }
+    }
+    if (!FILL && lane == 0) {
+        A.counts[sci] = n_ent;
+        A.counts[(A.nsci_i + 1) + sci] = n_cj;
+        A.counts[2 * (A.nsci_i + 1) + sci] = n_pool;
+    }
+}
+
+__global__ void k_pool0(nbx_mask_pool_entry* pool)
+{
+    int t = threadIdx.x;
+    if (t < 16) pool[0].m[t >> 1][t & 1] = (t & 1) ? 0u : 0xffffffffu;
+}
+
+// ---- prune ------------------------------------------------------------------------------
+struct PruneArgs {
+    const nbx_sci_entry* sci;
+    int n_sci, part, nparts;
+    const nbx_cj_entry* cj;
+    const nbx_mask_pool_entry* pool;
+    const float4* xq_i;
+    const float4* xq_j;
+    float3 box;
+    float rli2;
+    nbx_sci_entry* sci_in;
+    nbx_cj_entry* cj_in;
+};
+
+__global__ void __launch_bounds__(256) k_prune(PruneArgs A)
+{
+    const int lane = threadIdx.x & 31;
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int e = A.part + A.nparts * w;
+    if (e >= A.n_sci) return;
+    const unsigned lt = (1u << lane) - 1u;
+    const nbx_sci_entry se = A.sci[e];
+    const float3 v = shift_vec(se.shift, A.box);
+    const int i = lane >> 3, j = lane & 7;
+    float3 xi[8];
+#pragma unroll
+    for (int kk = 0; kk < 8; kk++) {
+        float4 t = A.xq_i[32 * se.sci + 4 * kk + i];
+        xi[kk] = make_float3(__fadd_rn(t.x, v.x), __fadd_rn(t.y, v.y), __fadd_rn(t.z, v.z));
+    }
+    int kept = 0;
+    for (int c0 = se.cj_start; c0 < se.cj_end; c0 += 32) {
+        nbx_cj_entry my;
+        my.cj = 0;
+        my.meta = 0u;
+        if (c0 + lane < se.cj_end) my = A.cj[c0 + lane];
+        const int nb = min(32, se.cj_end - c0);
+        unsigned mynew = 0u;
+        for (int t = 0; t < nb; t++) {
+            const int cj = __shfl_sync(0xffffffffu, my.cj, t);
+            const unsigned meta = __shfl_sync(0xffffffffu, my.meta, t);
+            const unsigned imask = meta & 0xffu, pidx = meta >> 8;
+            const float4 xj = A.xq_j[8 * cj + j];
+            unsigned nm = 0u;
+#pragma unroll
+            for (int kk = 0; kk < 8; kk++) {
+                if (imask & (1u << kk)) {
+                    unsigned pm = 0xffffffffu;
+                    if (pidx) pm = A.pool[pidx].m[kk][0] | A.pool[pidx].m[kk][1];
+                    const float dx = __fsub_rn(xi[kk].x, xj.x);
+                    const float dy = __fsub_rn(xi[kk].y, xj.y);
+                    const float dz = __fsub_rn(xi[kk].z, xj.z);
+                    const float r2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
+                    const bool hit = ((pm >> lane) & 1u) && (r2 < A.rli2);
+                    if (__any_sync(0xffffffffu, hit)) nm |= 1u << kk;
+                }
+            }
+            if (lane == t) mynew = nm;
+        }
+        const unsigned keep = __ballot_sync(0xffffffffu, mynew != 0u);
+        if (mynew) {
+            nbx_cj_entry o;
+            o.cj = my.cj;
+            o.meta = mynew | (my.meta & ~0xffu);
+            A.cj_in[se.cj_start + kept + __popc(keep & lt)] = o;
+        }
+        kept += __popc(keep);
+    }
+    if (lane == 0) {
+        nbx_sci_entry o = se;
+        o.cj_end = se.cj_start + kept;
+        A.sci_in[e] = o;
+    }
+}
+
+// count interacting in-cut-off pairs and pair slots of the inner list (bench denominator)
+__global__ void __launch_bounds__(256) k_count_pairs(PruneArgs A, float rc2, unsigned long long* out)
+{
+    const int lane = threadIdx.x & 31;
+    const int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (e >= A.n_sci) return;
+    const nbx_sci_entry se = A.sci_in[e];
+    const float3 v = shift_vec(se.shift, A.box);
+    const int i = lane >> 3, j = lane & 7;
+    unsigned long long np = 0, ns = 0;
+    for (int c = se.cj_start; c < se.cj_end; c++) {
+        const nbx_cj_entry ce = A.cj_in[c];
+        const unsigned imask = ce.meta & 0xffu, pidx = ce.meta >> 8;
+        const float4 xj = A.xq_j[8 * ce.cj + j];
+        for (int kk = 0; kk < 8; kk++) {
+            if (!(imask & (1u << kk))) continue;
+            const unsigned im = pidx ? A.pool[pidx].m[kk][0] : 0xffffffffu;
+            const float4 t = A.xq_i[32 * se.sci + 4 * kk + i];
+            const float dx = __fsub_rn(__fadd_rn(t.x, v.x), xj.x);
+            const float dy = __fsub_rn(__fadd_rn(t.y, v.y), xj.y);
+            const float dz = __fsub_rn(__fadd_rn(t.z, v.z), xj.z);
+            const float r2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
+            np += (((im >> lane) & 1u) && r2 < rc2) ? 1 : 0;
+            ns += 1;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) np += __shfl_xor_sync(0xffffffffu, np, o);
+    if (lane == 0) {
+        atomicAdd(&out[0], np);
+        atomicAdd(&out[1], ns);
+    }
+}
+
+void count_pairs(nbx_ctx* ctx, int l, long long* pairs, long long* slots, cudaStream_t st)
+{
+    List& L = ctx->list[l];
+    if (!L.built) throw CudaError{cudaErrorInvalidValue, "count before search"};
+    *pairs = 0;
+    *slots = 0;
+    if (L.n_sci == 0) return;
+    PruneArgs A;
+    A.sci = L.sci.p;
+    A.n_sci = (int)L.n_sci;
+    A.part = 0;
+    A.nparts = 1;
+    A.cj = L.cj.p;
+    A.pool = L.pool.p;
+    A.xq_i = ctx->grid[L.gi].xq.p;
+    A.xq_j = ctx->grid[L.gj].xq.p;
+    A.box = make_float3(ctx->box[0], ctx->box[1], ctx->box[2]);
+    A.rli2 = ctx->c.rli2;
+    A.sci_in = L.sci_in.p;
+    A.cj_in = L.cj_in.p;
+    DBuf<unsigned long long> out;
+    out.ensure(2);
+    NBX_CUDA(cudaMemsetAsync(out.p, 0, 2 * sizeof(unsigned long long), st));
+    k_count_pairs<<<(int)((L.n_sci * 32 + 255) / 256), 256, 0, st>>>(A, ctx->c.rc2, out.p);
+    ctx->launches++;
+    NBX_CUDA(cudaGetLastError());
+    unsigned long long h[2];
+    NBX_CUDA(cudaMemcpyAsync(h, out.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+    NBX_CUDA(cudaStreamSynchronize(st));
+    out.release();
+    *pairs = (long long)h[0];
+    *slots = 32ll * (long long)h[1];
+}
+
+void prune(nbx_ctx* ctx, int l, int part, int nparts, cudaStream_t st)
+{
+    List& L = ctx->list[l];
+    if (!L.built) throw CudaError{cudaErrorInvalidValue, "prune before search"};
+    if (L.n_sci == 0) return;
+    PruneArgs A;
+    A.sci = L.sci.p;
+    A.n_sci = (int)L.n_sci;
+    A.part = part;
+    A.nparts = nparts;
+    A.cj = L.cj.p;
+    A.pool = L.pool.p;
+    A.xq_i = ctx->grid[L.gi].xq.p;
+    A.xq_j = ctx->grid[L.gj].xq.p;
+    A.box = make_float3(ctx->box[0], ctx->box[1], ctx->box[2]);
+    A.rli2 = ctx->c.rli2;
+    A.sci_in = L.sci_in.p;
+    A.cj_in = L.cj_in.p;
+    const int nw = (int)((L.n_sci - part + nparts - 1) / nparts);
+    if (nw <= 0) return;
+    const int threads = 256;
+    k_prune<<<(nw * 32 + threads - 1) / threads, threads, 0, st>>>(A);
+    ctx->launches++;
+    NBX_CUDA(cudaGetLastError());
+}
+
+void search(nbx_ctx* ctx, int l, cudaStream_t st)
+{
+    List& L = ctx->list[l];
+    L.mode = l;
+    L.gi = 0;
+    L.gj = (l == NBX_LIST_LOCAL) ? 0 : 1;
+    Grid& GI = ctx->grid[L.gi];
+    Grid& GJ = ctx->grid[L.gj];
+    if (!GI.built || !GJ.built) throw CudaError{cudaErrorInvalidValue, "search before grid build"};
+    const int nsci = GI.nsci;
+    SearchArgs A;
+    A.bb_ci = GI.bb_ci.p;
+    A.bb_sci = GI.bb_sci.p;
+    A.order_i = GI.order.p;
+    A.gid_i = GI.gid.p;
+    A.exr_ci = GI.exr_ci.p;
+    A.nsci_i = nsci;
+    A.bb_cj = GJ.bb_cj.p;
+    A.bb_sci_j = GJ.bb_sci.p;
+    A.order_j = GJ.order.p;
+    A.gid_j = GJ.gid.p;
+    A.gr_cj = GJ.gr_cj.p;
+    A.col_start_j = GJ.col_start.p;
+    A.ncx_j = GJ.ncx;
+    A.ncy_j = GJ.ncy;
+    A.lo_jx = GJ.lo[0];
+    A.lo_jy = GJ.lo[1];
+    A.inv_jx = GJ.inv_cell[0];
+    A.inv_jy = GJ.inv_cell[1];
+    A.excl_off = ctx->excl_off_g.p;
+    A.excl_gid = ctx->excl_gid_g.p;
+    A.box = make_float3(ctx->box[0], ctx->box[1], ctx->box[2]);
+    A.pbc0 = ctx->pbc[0];
+    A.pbc1 = ctx->pbc[1];
+    A.pbc2 = ctx->pbc[2];
+    A.mode = L.mode;
+    A.rl = ctx->p.rlist_outer;
+    A.rl2 = ctx->c.rlo2;
+    A.rlm = ctx->p.rlist_outer * 1.001f + 1.0e-4f;
+
+    const int n3 = 3 * (nsci + 1);
+    L.counts.ensure(n3);
+    L.offsets.ensure(n3);
+    NBX_CUDA(cudaMemsetAsync(L.counts.p, 0, sizeof(int) * n3, st));
+    A.counts = L.counts.p;
+    A.offsets = L.offsets.p;
+    const int threads = 128;
+    const int blocks = (nsci * 32 + threads - 1) / threads;
+    if (nsci > 0) {
+        k_search<false><<<blocks, threads, 0, st>>>(A);
+        ctx->launches++;
+        NBX_CUDA(cudaGetLastError());
+    }
+    size_t tb = 0;
+    NBX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, L.counts.p, L.offsets.p, nsci + 1, st));
+    L.tmp.ensure(tb + 16);
+    for (int k = 0; k < 3; k++) {
+        NBX_CUDA(cub::DeviceScan::ExclusiveSum(L.tmp.p, tb, L.counts.p + k * (nsci + 1),
+                                               L.offsets.p + k * (nsci + 1), nsci + 1, st));
+        ctx->launches++;
+    }
+    int tot[3];
+    for (int k = 0; k < 3; k++)
+        NBX_CUDA(cudaMemcpyAsync(&tot[k], L.offsets.p + k * (nsci + 1) + nsci, sizeof(int),
+                                 cudaMemcpyDeviceToHost, st));
+    NBX_CUDA(cudaStreamSynchronize(st));
+    L.n_sci = tot[0];
+    L.n_cj = tot[1];
+    L.n_pool = (int64_t)tot[2] + 1;
+    if (L.n_pool >= (1ll << 24)) throw CudaError{cudaErrorMemoryAllocation, "mask pool exceeds 24-bit index"};
+    L.sci.ensure(L.n_sci + 1);
+    L.sci_in.ensure(L.n_sci + 1);
+    L.cj.ensure(L.n_cj + 1);
+    L.cj_in.ensure(L.n_cj + 1);
+    L.pool.ensure(L.n_pool);
+    A.sci_out = L.sci.p;
+    A.cj_out = L.cj.p;
+    A.pool_out = L.pool.p;
+    k_pool0<<<1, 32, 0, st>>>(L.pool.p);
+    ctx->launches++;
+    if (nsci > 0) {
+        k_search<true><<<blocks, threads, 0, st>>>(A);
+        ctx->launches++;
+        NBX_CUDA(cudaGetLastError());
+    }
+    L.built = true;
+    prune(ctx, l, 0, 1, st);
+}
+
+} // namespace nbx

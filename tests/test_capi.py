@@ -1,0 +1,69 @@
+"""CPU checks of the C-ABI boundary: libnbx.so loads, exports every symbol include/nbx.h
+declares, derives constants identically to the oracle, and fails loudly without a GPU."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2405_01420_b200 import nbx
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    txt = open(os.path.join(ROOT, "include", "nbx.h")).read()
+    return sorted(set(re.findall(r"NBX_API\s+[\w\s\*]+?\b(nbx_\w+)\s*\(", txt)))
+
+
+def test_header_symbols_listed():
+    assert header_symbols() == sorted(nbx.EXPORTS)
+
+
+def test_library_exports_every_symbol():
+    lib = C.CDLL(nbx.LIB_PATH)
+    for s in header_symbols():
+        assert hasattr(lib, s), f"{s} not exported by libnbx.so"
+
+
+def test_exports_are_only_the_abi():
+    out = os.popen(f"nm -D --defined-only {nbx.LIB_PATH}").read().split("\n")
+    syms = {l.split()[-1] for l in out if " T " in l}
+    assert {s for s in syms if s.startswith("nbx_")} == set(header_symbols())
+
+
+@pytest.mark.parametrize("kw", [dict(coulomb="rf", rc=0.9, rlist_outer=1.0, rlist_inner=0.92),
+                                dict(coulomb="ewald", rc=1.0, rlist_outer=1.1, rlist_inner=1.02),
+                                dict(coulomb="ewald", rc=1.2, rlist_outer=1.3, rlist_inner=1.22, ewald_rtol=1e-6),
+                                dict(coulomb="rf", rc=1.0, rlist_outer=1.2, rlist_inner=1.05, epsilon_r=2.0, epsilon_rf=78.0)])
+def test_derived_constants_bit_identical(kw):
+    a = nbx.derive_consts(nbx.make_params(**kw))
+    b = O.derive_consts(O.make_params(**kw))
+    for k in a:
+        assert np.float32(a[k]).tobytes() == np.float32(b[k]).tobytes(), k
+
+
+def test_invalid_params_rejected():
+    with pytest.raises(nbx.NbxError) as ei:
+        nbx.derive_consts(nbx.make_params(rc=1.0, rlist_outer=1.1, rlist_inner=0.9))
+    assert ei.value.code == 1
+
+
+def test_no_cpu_fallback():
+    """Without a usable sm_100 GPU, context creation fails with NBX_ECUDA -- never a CPU path."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(nbx.NbxError) as ei:
+        nbx.Context(nbx.make_params())
+    assert ei.value.code == 2
+    assert "no CPU fallback" in str(ei.value)
+
+
+def test_halo_entry_points_validate_arguments():
+    lib = nbx.lib()
+    assert lib.nbx_halo_pack_x(None, None, -1, None, None, None) == 1
+    assert lib.nbx_halo_unpack_add_f(None, None, 5, None, None) == 1
+    assert lib.nbx_halo_pack_x(None, None, 0, None, None, None) == 0
