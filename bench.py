@@ -1,0 +1,333 @@
+#!/usr/bin/env python
+"""bench.py -- NB-path MD steps of the B200-native NBNXM engine (libnbx.so).
+
+Metric (BASELINE.json): nonbonded pair-interactions/s and MD steps/s (ns/day) at 1/2/4/8
+B200 vs the FP32 roofline.  One "step" is one NB-path MD step with the reference cadence
+(pipeline.py:222-235): X buffer op + force kernel + F buffer op every step, the rolling
+prune every prune_every (10) steps, grid + pair search every nstlist (100) steps.  A step
+evaluates every in-cut-off pair once, so pair-interactions/s = pairs_per_step * steps / s.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config water12m] [--impl nbx|reference]
+
+N = 1: single domain on cuda:0.  N > 1 (torchrun, one rank per GPU): spatial domain
+decomposition (paper_2405_01420_b200.dd) with NCCL halo exchange; strong scaling (the box is
+fixed).  `--impl reference` times the CPU implementation of the path (the C oracle port,
+all host threads, rank 0 only) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "nonbonded pair-interactions/s and MD steps/s (ns/day) at 1/2/4/8 B200 vs FP32 roofline"
+UNIT = "pair-interactions/s"
+# Algorithmic FP32 flops per in-cut-off pair of the force-only kernel, counted once from
+# pairmath.cuh / force.cu (FADD/FMUL/MUFU = 1, FFMA = 2) and frozen.
+FLOPS_PER_PAIR = {"ewald": 57, "rf": 33}
+DESC = {
+    "water3k": "SPC/E water box 3k atoms (1k waters), reaction-field, rc=0.9 nm",
+    "rnase24k": "RNase-sized 24,024-atom solvated protein-like box, Ewald real-space, rc=1.0 nm",
+    "mem82k": "benchMEM-sized 82k-atom membrane-like box, LJ + Ewald, dynamic pruning every 10 steps",
+    "stmv": "STMV-sized 1,066,628-atom water/protein box, Ewald, rc=1.2 nm",
+    "water12m": "12M-atom water box, Ewald, rc=1.0 nm (strong-scaling sweep 1/2/4/8)",
+}
+L2_BYTES = 126 * 1024 * 1024
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="water12m", choices=sorted(DESC))
+    ap.add_argument("--impl", default="nbx", choices=["nbx", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded CPU baseline budget")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.f = None
+
+    def start(self):
+        try:
+            self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.index), "-lms", "100"], stdout=self.f,
+                                         stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def stop(self):
+        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        if self.proc is None:
+            return out
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.flush()
+        self.f.seek(0)
+        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        clocks, maxc, reasons, power = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                clocks.append(float(r[1]))
+                maxc.append(float(r[2]))
+                power.append(float(r[3]))
+                for k, nm in enumerate(names):
+                    if r[5 + k].strip().lower() == "active":
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                continue
+        if clocks:
+            busy = sorted(c for c in clocks if c > 0.5 * max(clocks)) or sorted(clocks)
+            out = {"sm_mhz": busy[len(busy) // 2], "sm_max_mhz": max(maxc), "reasons": sorted(reasons),
+                   "samples": len(clocks), "power_w_max": max(power) if power else None}
+        return out
+
+
+# ------------------------------------------------------------------------------ helpers
+def dist_env():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(
+        os.environ.get("LOCAL_RANK", "0"))
+
+
+def load_traffic(config, n):
+    """dram bytes per force launch from the committed ncu --set full capture, if any."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get(f"{config}:{n}")
+    except Exception:
+        return None
+
+
+def cpu_sample_system(config):
+    """A bounded sample of the workload for the CPU port: same generator/parameters, fewer atoms."""
+    from paper_2405_01420_b200 import systems
+    n = {"water3k": None, "rnase24k": None, "mem82k": 24000, "stmv": 48000, "water12m": 48000}[config]
+    return systems.make(config, n), n
+
+
+def time_cpu_port(config, budget_s, steps=None, warmup=0):
+    """Oracle port (C, OpenMP, all host threads) on the bounded sample: pairs/s."""
+    from oracle import oracle as O
+    s, n = cpu_sample_system(config)
+    on = O.OracleNonbonded(s)
+    on.search(s.x)
+    pairs = on.count_pairs()
+    cores = len(os.sched_getaffinity(0))
+    on.forces(flags=0)  # warm the thread pool / caches
+    for _ in range(warmup):
+        on.forces(flags=0)
+    t0 = time.perf_counter()
+    reps = 0
+    times = []
+    while True:
+        t = time.perf_counter()
+        on.forces(flags=0)
+        times.append(time.perf_counter() - t)
+        reps += 1
+        if steps is not None and reps >= steps:
+            break
+        if steps is None and (time.perf_counter() - t0) >= budget_s:
+            break
+    tot = sum(times)
+    sample = (f"C oracle force evaluation (F only, Ewald/RF as configured) on a {s.natoms}-atom box "
+              f"of the same generator and parameters ({reps} evaluations, {pairs} pairs each)")
+    return {"value": pairs * reps / tot, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
+            "ms_per_eval": 1e3 * tot / reps, "pairs_per_eval": pairs, "reps": reps}
+
+
+# ------------------------------------------------------------------------------ nbx arm, N = 1
+def run_single(args):
+    import numpy as np
+    import torch
+
+    from paper_2405_01420_b200 import nbx, systems
+
+    torch.cuda.set_device(0)
+    s = systems.make(args.config)
+    nb = nbx.Nonbonded(s, device=0)
+    x = torch.from_numpy(s.x).cuda()
+    f = torch.empty_like(x)
+    st = torch.cuda.current_stream()
+    peak = nb.fma_peak_tflops()
+
+    # warm-up steps 0..W-1 (step 0 is a search step)
+    for k in range(args.warmup):
+        nb.step(x, f, k)
+    torch.cuda.synchronize()
+    pairs, slots = nb.count_pairs()
+    sizes = nb.list_sizes()
+    nslots = nb.grid_info()["nslots"]
+    working = nslots * 16 * 3 + sizes["n_cj_outer"] * 16 + sizes["n_pool"] * 64
+    flush = working < 2 * L2_BYTES
+    scratch = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device="cuda") if flush else None
+
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    evf = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    clocks = ClockSampler(0).start()
+    torch.cuda.synchronize()
+    l0 = nb.launch_count()
+    n_search = n_prune = 0
+    for k in range(K):
+        step = args.warmup + k
+        if flush:
+            scratch.fill_(float(k))
+        ev[k][0].record(st)
+        search = step % s.nstlist == 0
+        prune = (not search) and s.prune_every and step % s.prune_every == 0
+        if search:
+            nb.search(x)
+            n_search += 1
+        else:
+            nb.put_x(x)
+            if prune:
+                nb.prune()
+                n_prune += 1
+        evf[k][0].record(st)
+        nb.compute()
+        evf[k][1].record(st)
+        nb.get_f(f)
+        ev[k][1].record(st)
+    torch.cuda.synchronize()
+    launches = nb.launch_count() - l0
+    clk = clocks.stop()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    force_ms = [a.elapsed_time(b) for a, b in evf]
+    tot_ms = sum(step_ms)
+    ms_per_step = tot_ms / K
+    value = pairs * K / (tot_ms * 1e-3)
+    t_force = sum(force_ms) / K
+    fl = FLOPS_PER_PAIR[s.coulomb]
+    achieved = pairs * fl / (t_force * 1e-3) / 1e12
+    slot_tf = slots * fl / (t_force * 1e-3) / 1e12
+
+    # e2e: public API with host buffers, H2D of x and D2H of f inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        xh = torch.from_numpy(s.x.copy()).pin_memory()
+        fh = torch.empty((s.natoms, 3), dtype=torch.float32).pin_memory()
+        xd = torch.empty_like(x)
+        Ke = max(1, min(K, 50))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(st)
+        for k in range(Ke):
+            step = args.warmup + K + k
+            xd.copy_(xh, non_blocking=True)
+            nb.step(xd, f, step)
+            fh.copy_(f, non_blocking=True)
+        e1.record(st)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        e2e = {"value": pairs * Ke / (ems * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(xh.numel() * 4),
+               "d2h_bytes_per_step": int(fh.numel() * 4), "steps": Ke, "ms_per_step": ems / Ke,
+               "api": "paper_2405_01420_b200.nbx.Nonbonded.step (ctypes -> libnbx.so C-ABI)"}
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        try:
+            cpu = time_cpu_port(args.config, args.cpu_seconds)
+        except Exception as e:  # reported, never substituted
+            cpu = {"value": None, "error": str(e)[:200]}
+
+    traffic = load_traffic(args.config, 1)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": K, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {DESC[args.config]}", "natoms": s.natoms,
+                   "nstlist": s.nstlist, "prune_every": s.prune_every, "rc": s.rc,
+                   "rlist_outer": s.rlist_outer, "rlist_inner": s.rlist_inner,
+                   "parallelism": "single domain",
+                   "l2": ("L2 flushed (2x126 MB write) before every timed step" if flush
+                          else f"inputs larger than L2 (xyzq+lists {working / 2**20:.0f} MiB)")},
+        "steps_per_s": 1e3 / ms_per_step,
+        "ns_per_day": 86.4 * s.dt_fs / ms_per_step,
+        "pairs_per_step": pairs,
+        "pair_slots_per_step": slots,
+        "cluster_efficiency": pairs / slots if slots else None,
+        "kernels_ms": {"force_avg": t_force, "step_avg": ms_per_step,
+                       "searches": n_search, "prunes": n_prune},
+        "roofline": {"bound": "fp32", "kernel": "k_force (NBNXM force, F only)", "achieved": achieved,
+                     "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                     "peak_source": "measured on this GPU: register-resident FFMA loop (nbx_fma_peak)",
+                     "flops_per_pair": fl, "slot_tflops": slot_tf, "slot_frac": slot_tf / peak},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------ reference arm
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2405_01420_b200 import systems
+    full = systems.make(args.config) if args.config in ("water3k", "rnase24k") else None
+    t0 = time.perf_counter()
+    r = time_cpu_port(args.config, None, steps=args.steps, warmup=args.warmup)
+    wall = time.perf_counter() - t0
+    line = {
+        "impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms_per_eval"], "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {DESC[args.config]}",
+                   "natoms": full.natoms if full is not None else None,
+                   "parallelism": "host CPU (reference path has no GPU implementation)"},
+        "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "port",
+                         "sample": r["sample"]},
+        "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": ("the reference (mdgpusim) computes no forces (SPEC.md:8); this arm times the CPU "
+                 "restatement of the path (oracle/nbx_oracle.c) on the box's host cores"),
+        "wall_s": wall,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    rank, world, local = dist_env()
+    if world > 1 or args.gpus > 1:
+        from paper_2405_01420_b200 import dd
+        dd.bench(args, METRIC, UNIT, FLOPS_PER_PAIR, DESC, ClockSampler, time_cpu_port, load_traffic)
+        return
+    run_single(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,429 @@
+"""Spatial domain decomposition of the NB path over 2/4/8 GPUs.
+
+Reference shape (/root/reference/pkg/src/mdgpusim/pipeline.py:267-438): near-cubic rank grid
+`balanced_dims` (pipeline.py:42-60; 2 -> (2,1,1), 4 -> (2,2,1), 8 -> (2,2,2)), one halo pulse
+per split dimension (pipeline.py:273-278, 363-380), the local force kernel overlapping the
+coordinate halo (pipeline.py:344-349), the nonlocal kernel after the unpack
+(pipeline.py:382-388) and the reverse force halo (pipeline.py:403-418).  There it is all
+simulated time; here it is real:
+
+  * one process per GPU, `torch.distributed` over NCCL; halo messages are stream-ordered
+    point-to-point sends/receives batched per pulse (no host sync, unlike the paper's
+    CPU-initiated MPI);
+  * halo width = rlist_outer, staged pulses x -> y -> z forward edge/corner atoms;
+    every rank imports the full shell (both faces of each split dimension);
+  * every cross-domain pair is computed exactly once, on the rank whose home atom has the
+    smaller global id (the nonlocal list's masks encode it, include/nbx.h NBX_LIST_NONLOCAL);
+    forces on imported atoms go back through the reverse pulses and are accumulated by
+    the owner (z -> y -> x);
+  * atoms are (re)assigned to domains at search steps from the global coordinates.
+
+The per-rank engine is libnbx (`NbxEngine`); the host logic takes any object with the same
+methods so the multi-process logic is also testable on CPU with gloo (tests/test_dd.py).
+"""
+from __future__ import annotations
+
+import json
+import math
+import os
+import time
+
+import numpy as np
+
+
+def balanced_dims(n: int):
+    """Same factorisation as the reference's pipeline.balanced_dims (pipeline.py:42-60)."""
+    if n < 1:
+        raise ValueError("need at least one rank")
+    best = (n, 1, 1)
+    for dz in range(1, int(round(n ** (1 / 3))) + 1):
+        if n % dz:
+            continue
+        rest = n // dz
+        for dy in range(dz, int(rest**0.5) + 1):
+            if rest % dy:
+                continue
+            dx = rest // dy
+            if dx >= dy and (dx - dz) < (max(best) - min(best)):
+                best = (dx, dy, dz)
+    return best
+
+
+def rank_coords(rank, dims):
+    return (rank % dims[0], (rank // dims[0]) % dims[1], rank // (dims[0] * dims[1]))
+
+
+def coords_rank(c, dims):
+    return (c[0] % dims[0]) + dims[0] * ((c[1] % dims[1]) + dims[1] * (c[2] % dims[2]))
+
+
+class NbxEngine:
+    """Per-rank libnbx context with a local (home) and a nonlocal (halo) grid."""
+
+    def __init__(self, system, device, pbc):
+        import torch
+
+        from . import nbx
+        self.torch = torch
+        self.nbx = nbx
+        self.device = device
+        self.params = nbx.make_params(**system.params())
+        self.ctx = nbx.Context(self.params, device)
+        q = np.ascontiguousarray(system.q, np.float32)
+        t = np.ascontiguousarray(system.type, np.int32)
+        c6c12 = np.ascontiguousarray(system.c6c12, np.float32)
+        eo = np.ascontiguousarray(system.excl_offsets, np.int32)
+        eg = np.ascontiguousarray(system.excl_gids, np.int32)
+        L = nbx.lib()
+        nbx.check(L.nbx_set_topology(self.ctx.h, system.natoms, nbx._ptr(q), nbx._ptr(t), int(c6c12.shape[0]),
+                                     nbx._ptr(c6c12), nbx._ptr(eo), nbx._ptr(eg)))
+        self.box = np.ascontiguousarray(system.box, np.float32)
+        self.pbc = np.ascontiguousarray(pbc, np.int32)
+        nbx.check(L.nbx_set_box(self.ctx.h, nbx._ptr(self.box), nbx._ptr(self.pbc)))
+
+    def _st(self, stream=None):
+        return self.nbx._stream(self.torch, stream)
+
+    def grid_build(self, g, x, gid, lo, size):
+        nbx = self.nbx
+        lo = np.ascontiguousarray(lo, np.float32)
+        size = np.ascontiguousarray(size, np.float32)
+        n = int(x.shape[0])
+        nbx.check(nbx.lib().nbx_grid_build(self.ctx.h, g, n, nbx._dev_ptr(x) if n else None,
+                                           nbx._dev_ptr(gid) if n else None, nbx._ptr(lo), nbx._ptr(size),
+                                           self._st()))
+
+    def search(self, lst):
+        self.nbx.check(self.nbx.lib().nbx_search(self.ctx.h, lst, self._st()))
+
+    def put_x(self, g, x, stream=None):
+        if x.shape[0]:
+            self.nbx.check(self.nbx.lib().nbx_put_x(self.ctx.h, g, self.nbx._dev_ptr(x), self._st(stream)))
+
+    def prune(self, lst, stream=None):
+        self.nbx.check(self.nbx.lib().nbx_prune(self.ctx.h, lst, 0, 1, self._st(stream)))
+
+    def force(self, lst, flags, stream=None):
+        self.nbx.check(self.nbx.lib().nbx_force(self.ctx.h, lst, flags, self._st(stream)))
+
+    def get_f(self, g, f, accumulate=False, stream=None):
+        if f.shape[0]:
+            self.nbx.check(self.nbx.lib().nbx_get_f(self.ctx.h, g, self.nbx._dev_ptr(f), 1 if accumulate else 0,
+                                                    self._st(stream)))
+
+    def clear_energies(self, stream=None):
+        self.nbx.check(self.nbx.lib().nbx_clear_energies(self.ctx.h, self._st(stream)))
+
+    def energies(self, stream=None):
+        e = np.zeros(2)
+        v = np.zeros(9)
+        self.nbx.check(self.nbx.lib().nbx_energies(self.ctx.h, self.nbx._ptr(e), self.nbx._ptr(v), self._st(stream)))
+        return e, v
+
+    def count_pairs(self, lst):
+        import ctypes as C
+        p, s = C.c_int64(), C.c_int64()
+        self.nbx.check(self.nbx.lib().nbx_count_pairs(self.ctx.h, lst, C.byref(p), C.byref(s), self._st()))
+        return p.value, s.value
+
+    def halo_pack(self, x, idx, shift, out, stream=None):
+        nbx = self.nbx
+        n = int(idx.shape[0])
+        if n:
+            sh = np.ascontiguousarray(shift, np.float32)
+            nbx.check(nbx.lib().nbx_halo_pack_x(nbx._dev_ptr(x), nbx._dev_ptr(idx), n, nbx._ptr(sh),
+                                                nbx._dev_ptr(out), self._st(stream)))
+
+    def halo_unpack_add(self, f, idx, buf, stream=None):
+        nbx = self.nbx
+        n = int(idx.shape[0])
+        if n:
+            nbx.check(nbx.lib().nbx_halo_unpack_add_f(nbx._dev_ptr(f), nbx._dev_ptr(idx), n, nbx._dev_ptr(buf),
+                                                      self._st(stream)))
+
+    def launch_count(self):
+        return self.nbx.lib().nbx_launch_count(self.ctx.h)
+
+    def fma_peak(self):
+        import ctypes as C
+        v = C.c_double()
+        self.nbx.check(self.nbx.lib().nbx_fma_peak(self.ctx.h, C.byref(v), self._st()))
+        return v.value
+
+
+class Pulse:
+    __slots__ = ("dim", "down_peer", "up_peer", "down_idx", "up_idx", "shift_down", "shift_up",
+                 "n_from_up", "n_from_down", "off_from_up", "off_from_down")
+
+
+class DomainDecomposition:
+    """One rank of the DD NB path.  `engine` is NbxEngine (GPU) or a test double."""
+
+    def __init__(self, system, rank, world, engine_factory, device=None, group=None):
+        import torch
+        import torch.distributed as dist
+
+        self.torch = torch
+        self.dist = dist
+        self.sys = system
+        self.rank, self.world = rank, world
+        self.group = group
+        self.dims = balanced_dims(world)
+        self.coord = rank_coords(rank, self.dims)
+        self.box = np.asarray(system.box, np.float64)
+        self.D = self.box / np.array(self.dims)
+        self.rl = float(system.rlist_outer)
+        for d in range(3):
+            if self.dims[d] > 1 and self.D[d] < 2 * self.rl:
+                raise ValueError(f"domain width {self.D[d]:.3f} nm < 2*rlist_outer in dim {d}")
+        self.pbc = [1 if self.dims[d] == 1 else 0 for d in range(3)]
+        self.device = device if device is not None else torch.device("cpu")
+        self.engine = engine_factory(system, self.pbc)
+        self.pulses = []
+        self.n_home = 0
+        self.n_ext = 0
+        self.nstlist = system.nstlist
+        self.prune_every = system.prune_every
+        self.comm_stream = None
+
+    # ---------------------------------------------------------------------- partitioning
+    def _exchange(self, sends, recvs):
+        """One batched NCCL/gloo point-to-point group: sends/recvs are (tensor, peer) lists."""
+        dist = self.dist
+        ops = [dist.P2POp(dist.isend, t, p, group=self.group) for t, p in sends if t.numel()]
+        ops += [dist.P2POp(dist.irecv, t, p, group=self.group) for t, p in recvs if t.numel()]
+        if not ops:
+            return []
+        return dist.batch_isend_irecv(ops)
+
+    def repartition(self, x_global):
+        """Assign home atoms, build the halo plan, grids and lists (a search step)."""
+        torch = self.torch
+        dev = self.device
+        box = torch.tensor(self.box, dtype=torch.float32, device=dev)
+        xg = x_global.to(dev, torch.float32)
+        xw = xg - torch.floor(xg / box) * box
+        D = torch.tensor(self.D, dtype=torch.float32, device=dev)
+        cidx = torch.clamp(torch.floor(xw / D).to(torch.int64), min=0)
+        dims_t = torch.tensor(self.dims, dtype=torch.int64, device=dev)
+        cidx = torch.minimum(cidx, dims_t - 1)
+        owner = cidx[:, 0] + self.dims[0] * (cidx[:, 1] + self.dims[1] * cidx[:, 2])
+        home = torch.nonzero(owner == self.rank).flatten()
+        self.home_gid = home.to(torch.int32)
+        self.n_home = int(home.numel())
+        X = xw[home].contiguous()
+        G = self.home_gid.clone()
+        lo = np.array([self.coord[d] * self.D[d] for d in range(3)])
+        self.lo = lo
+        self.pulses = []
+        for d in range(3):
+            n_d = self.dims[d]
+            if n_d == 1:
+                continue
+            p = Pulse()
+            p.dim = d
+            c = list(self.coord)
+            c[d] = self.coord[d] - 1
+            p.down_peer = coords_rank(c, self.dims)
+            c[d] = self.coord[d] + 1
+            p.up_peer = coords_rank(c, self.dims)
+            lo_d, hi_d = lo[d], lo[d] + self.D[d]
+            p.down_idx = torch.nonzero(X[:, d] < lo_d + self.rl).flatten().to(torch.int32)
+            p.up_idx = torch.nonzero(X[:, d] >= hi_d - self.rl).flatten().to(torch.int32)
+            sd = np.zeros(3, np.float32)
+            su = np.zeros(3, np.float32)
+            if self.coord[d] == 0:
+                sd[d] = self.box[d]
+            if self.coord[d] == n_d - 1:
+                su[d] = -self.box[d]
+            p.shift_down, p.shift_up = sd, su
+            # sizes
+            cnt_send = torch.tensor([p.down_idx.numel(), p.up_idx.numel()], dtype=torch.int64, device=dev)
+            cnt_from_up = torch.zeros(2, dtype=torch.int64, device=dev)
+            cnt_from_down = torch.zeros(2, dtype=torch.int64, device=dev)
+            for w in self._exchange([(cnt_send, p.down_peer), (cnt_send, p.up_peer)],
+                                    [(cnt_from_up, p.up_peer), (cnt_from_down, p.down_peer)]):
+                w.wait()
+            p.n_from_up = int(cnt_from_up[0])  # the up neighbour's down set
+            p.n_from_down = int(cnt_from_down[1])  # the down neighbour's up set
+            n0 = X.shape[0]
+            p.off_from_up, p.off_from_down = n0, n0 + p.n_from_up
+            send_d = (X[p.down_idx.long()] + torch.from_numpy(sd).to(dev)).contiguous()
+            send_u = (X[p.up_idx.long()] + torch.from_numpy(su).to(dev)).contiguous()
+            recv_u = torch.empty((p.n_from_up, 3), dtype=torch.float32, device=dev)
+            recv_d = torch.empty((p.n_from_down, 3), dtype=torch.float32, device=dev)
+            gsd, gsu = G[p.down_idx.long()].contiguous(), G[p.up_idx.long()].contiguous()
+            gru = torch.empty(p.n_from_up, dtype=torch.int32, device=dev)
+            grd = torch.empty(p.n_from_down, dtype=torch.int32, device=dev)
+            for w in self._exchange([(send_d, p.down_peer), (send_u, p.up_peer), (gsd, p.down_peer),
+                                     (gsu, p.up_peer)],
+                                    [(recv_u, p.up_peer), (recv_d, p.down_peer), (gru, p.up_peer),
+                                     (grd, p.down_peer)]):
+                w.wait()
+            X = torch.cat([X, recv_u, recv_d])
+            G = torch.cat([G, gru, grd])
+            self.pulses.append(p)
+        self.n_ext = X.shape[0]
+        self.x_ext = X.contiguous()
+        self.gid_ext = G.contiguous()
+        self.f_ext = torch.zeros_like(self.x_ext)
+        self.fbuf_down = [torch.empty((p.down_idx.numel(), 3), dtype=torch.float32, device=dev) for p in self.pulses]
+        self.fbuf_up = [torch.empty((p.up_idx.numel(), 3), dtype=torch.float32, device=dev) for p in self.pulses]
+        self.xbuf_down = [torch.empty((p.down_idx.numel(), 3), dtype=torch.float32, device=dev) for p in self.pulses]
+        self.xbuf_up = [torch.empty((p.up_idx.numel(), 3), dtype=torch.float32, device=dev) for p in self.pulses]
+        # grids: local = home atoms over the home domain (periodic only in undivided dims),
+        # nonlocal = imported atoms over the domain grown by rlist in split dims
+        size_l = np.array([self.D[d] if self.dims[d] > 1 else self.box[d] for d in range(3)], np.float32)
+        lo_l = np.array([lo[d] if self.dims[d] > 1 else 0.0 for d in range(3)], np.float32)
+        size_n = np.array([self.D[d] + 2 * self.rl if self.dims[d] > 1 else self.box[d] for d in range(3)], np.float32)
+        lo_n = np.array([lo[d] - self.rl if self.dims[d] > 1 else 0.0 for d in range(3)], np.float32)
+        eng = self.engine
+        eng.grid_build(0, self.x_ext[:self.n_home], self.gid_ext[:self.n_home], lo_l, size_l)
+        eng.search(0)
+        eng.grid_build(1, self.x_ext[self.n_home:], self.gid_ext[self.n_home:], lo_n, size_n)
+        eng.search(1)
+        return self.n_home
+
+    # ---------------------------------------------------------------------- per step
+    def halo_x(self):
+        """Coordinate halo: pack with shift, exchange per pulse, received straight in place."""
+        eng = self.engine
+        works = []
+        for k, p in enumerate(self.pulses):
+            for w in works:
+                w.wait()  # pulse k forwards atoms received in pulse k-1
+            eng.halo_pack(self.x_ext, p.down_idx, p.shift_down, self.xbuf_down[k])
+            eng.halo_pack(self.x_ext, p.up_idx, p.shift_up, self.xbuf_up[k])
+            ru = self.x_ext[p.off_from_up:p.off_from_up + p.n_from_up]
+            rd = self.x_ext[p.off_from_down:p.off_from_down + p.n_from_down]
+            works = self._exchange([(self.xbuf_down[k], p.down_peer), (self.xbuf_up[k], p.up_peer)],
+                                   [(ru, p.up_peer), (rd, p.down_peer)])
+        return works
+
+    def halo_f(self):
+        """Force halo: reverse pulses z -> y -> x, accumulated into the owner's atoms."""
+        eng = self.engine
+        for k in range(len(self.pulses) - 1, -1, -1):
+            p = self.pulses[k]
+            fu = self.f_ext[p.off_from_up:p.off_from_up + p.n_from_up]
+            fd = self.f_ext[p.off_from_down:p.off_from_down + p.n_from_down]
+            for w in self._exchange([(fu, p.up_peer), (fd, p.down_peer)],
+                                    [(self.fbuf_down[k], p.down_peer), (self.fbuf_up[k], p.up_peer)]):
+                w.wait()
+            eng.halo_unpack_add(self.f_ext, p.down_idx, self.fbuf_down[k])
+            eng.halo_unpack_add(self.f_ext, p.up_idx, self.fbuf_up[k])
+
+    def step(self, x_home=None, step=1, energy=False, virial=False, prune=None):
+        """One NB-path step (non-search): returns f_home view (and energies/virial if asked)."""
+        eng = self.engine
+        if x_home is not None:
+            self.x_ext[:self.n_home].copy_(x_home)
+        if prune is None:
+            prune = bool(self.prune_every) and step % self.prune_every == 0
+        works = self.halo_x()  # NCCL in flight while the local kernel runs
+        eng.put_x(0, self.x_ext[:self.n_home])
+        if prune:
+            eng.prune(0)
+        flags = (1 if energy else 0) | (2 if virial else 0)
+        if flags:
+            eng.clear_energies()
+        eng.force(0, flags)
+        for w in works:
+            w.wait()
+        eng.put_x(1, self.x_ext[self.n_home:])
+        if prune:
+            eng.prune(1)
+        eng.force(1, flags)
+        res = None
+        if flags:
+            e, v = eng.energies()
+            t = self.torch.tensor(np.concatenate([e, v]), dtype=self.torch.float64, device=self.device)
+            self.dist.all_reduce(t, group=self.group)
+            t = t.cpu().numpy()
+            res = (t[:2], t[2:].reshape(3, 3))
+        eng.get_f(0, self.f_ext[:self.n_home])
+        eng.get_f(1, self.f_ext[self.n_home:])
+        self.halo_f()
+        f_home = self.f_ext[:self.n_home]
+        return (f_home, res) if res is not None else f_home
+
+    def count_pairs(self):
+        p0, s0 = self.engine.count_pairs(0)
+        p1, s1 = self.engine.count_pairs(1)
+        return p0 + p1, s0 + s1
+
+
+# ---------------------------------------------------------------------------- bench, N > 1
+def bench(args, METRIC, UNIT, FLOPS_PER_PAIR, DESC, ClockSampler, time_cpu_port, load_traffic):
+    import torch
+    import torch.distributed as dist
+
+    from . import systems
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    s = systems.make(args.config)
+    dd = DomainDecomposition(s, rank, world, lambda sy, pbc: NbxEngine(sy, local, pbc), device=dev)
+    xg = torch.from_numpy(s.x).to(dev)
+    peak = dd.engine.fma_peak()
+    dd.repartition(xg)
+    x_home = dd.x_ext[:dd.n_home].clone()
+    for k in range(1, args.warmup):
+        dd.step(x_home, step=k)
+    torch.cuda.synchronize()
+    pairs, slots = dd.count_pairs()
+    pt = torch.tensor([pairs, slots], dtype=torch.float64, device=dev)
+    dist.all_reduce(pt)
+    pairs_tot, slots_tot = float(pt[0]), float(pt[1])
+
+    K = args.steps
+    st = torch.cuda.current_stream()
+    clocks = ClockSampler(local).start()
+    dist.barrier()
+    torch.cuda.synchronize()
+    l0 = dd.engine.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    n_search = 0
+    for k in range(K):
+        step = args.warmup + k
+        if step % s.nstlist == 0:
+            dd.repartition(xg)  # atoms re-assigned from the global coordinates
+            n_search += 1
+            x_home = dd.x_ext[:dd.n_home].clone()
+            dd.step(None, step=step, prune=False)
+        else:
+            dd.step(x_home, step=step)
+    e1.record(st)
+    torch.cuda.synchronize()
+    dist.barrier()
+    launches = dd.engine.launch_count() - l0
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t[0])
+    clk = clocks.stop()
+    if rank == 0:
+        ms_per_step = ms_max / K
+        value = pairs_tot * K / (ms_max * 1e-3)
+        fl = FLOPS_PER_PAIR[s.coulomb]
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {DESC[args.config]}", "natoms": s.natoms,
+                       "parallelism": f"spatial DD {dd.dims[0]}x{dd.dims[1]}x{dd.dims[2]}, NCCL P2P halo",
+                       "nstlist": s.nstlist, "prune_every": s.prune_every,
+                       "l2": "inputs larger than L2" if s.natoms > 2_000_000 else "per-rank inputs may fit L2"},
+            "steps_per_s": 1e3 / ms_per_step, "ns_per_day": 86.4 * s.dt_fs / ms_per_step,
+            "pairs_per_step": pairs_tot, "pair_slots_per_step": slots_tot,
+            "roofline": {"bound": "fp32", "achieved": value / 1e12 * fl / world, "peak": peak, "unit": "TFLOP/s",
+                         "frac": value / 1e12 * fl / world / peak, "traffic": load_traffic(args.config, world),
+                         "note": "per GPU, whole NB step (not kernel-only) at N>1"},
+            "e2e": None, "gpu_launches": int(launches), "clocks": clk, "searches": n_search,
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
