@@ -81,6 +81,7 @@ struct SlabArgs {
     int* type;
     float4* xq;
     float4* wrapk;
+    int* slotmap;
 };
 
 // rank of this lane's key among the real lanes of the same group (ties impossible: idx)
@@ -137,6 +138,7 @@ __global__ void k_slab(SlabArgs A)
         A.type[slot] = A.type_g[g];
         A.xq[slot] = make_float4(w.x, w.y, w.z, q);
         A.wrapk[slot] = make_float4(k.x, k.y, k.z, q);
+        A.slotmap[g] = slot;
     }
     if (!((occ >> lane) & 1u)) {
         int slot = slot0 + lane;
@@ -153,13 +155,9 @@ struct BBArgs {
     const int* order;
     const int* gid;
     const float4* xq;
-    const int* excl_off;
-    const int* excl_gid;
     float4* bb_ci;
     float4* bb_cj;
     float4* bb_sci;
-    int2* exr_ci;
-    int2* gr_cj;
     double* sumq2;
 };
 
@@ -176,14 +174,6 @@ __device__ __forceinline__ void bb_reduce(float3& lo, float3& hi, int& nr, int x
     }
 }
 
-__device__ __forceinline__ void range_reduce(int& lo, int& hi, int x0, int x1)
-{
-    for (int o = x0; o <= x1; o <<= 1) {
-        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-    }
-}
-
 __global__ void k_bbox(BBArgs A, int gslot)
 {
     const int lane = threadIdx.x & 31;
@@ -195,33 +185,18 @@ __global__ void k_bbox(BBArgs A, int gslot)
     float3 lo = real ? make_float3(x.x, x.y, x.z) : make_float3(NBX_BB_EMPTY, NBX_BB_EMPTY, NBX_BB_EMPTY);
     float3 hi = real ? make_float3(x.x, x.y, x.z) : make_float3(-NBX_BB_EMPTY, -NBX_BB_EMPTY, -NBX_BB_EMPTY);
     int nr = real ? 1 : 0;
-    int elo = 0x7fffffff, ehi = -1, glo = 0x7fffffff, ghi = -1;
-    double q2 = 0.0;
-    if (real) {
-        int g = A.gid[slot];
-        glo = ghi = g;
-        for (int e = A.excl_off[g]; e < A.excl_off[g + 1]; e++) {
-            int p = A.excl_gid[e];
-            elo = min(elo, p);
-            ehi = max(ehi, p);
-        }
-        q2 = (double)x.w * (double)x.w;
-    }
+    double q2 = real ? (double)x.w * (double)x.w : 0.0;
     bb_reduce(lo, hi, nr, 1, 2);
-    range_reduce(elo, ehi, 1, 2);
-    range_reduce(glo, ghi, 1, 4);
     if ((lane & 3) == 0) {
         int ci = 8 * s + (lane >> 2);
         A.bb_ci[2 * ci] = make_float4(lo.x, lo.y, lo.z, (float)nr);
         A.bb_ci[2 * ci + 1] = make_float4(hi.x, hi.y, hi.z, 0.f);
-        A.exr_ci[ci] = make_int2(elo, ehi);
     }
     bb_reduce(lo, hi, nr, 4, 4);
     if ((lane & 7) == 0) {
         int cj = 4 * s + (lane >> 3);
         A.bb_cj[2 * cj] = make_float4(lo.x, lo.y, lo.z, (float)nr);
         A.bb_cj[2 * cj + 1] = make_float4(hi.x, hi.y, hi.z, 0.f);
-        A.gr_cj[cj] = make_int2(glo, ghi);
     }
     bb_reduce(lo, hi, nr, 8, 16);
     for (int o = 16; o > 0; o >>= 1) q2 += __shfl_xor_sync(0xffffffffu, q2, o);
@@ -316,7 +291,8 @@ void grid_build(nbx_ctx* ctx, int g, int n, const float* x, const int* gid, cons
     G.order.ensure(ns); G.gid.ensure(ns); G.type.ensure(ns);
     G.xq.ensure(ns); G.wrapk.ensure(ns); G.f.ensure(ns);
     G.bb_ci.ensure(2 * (ns / 4)); G.bb_cj.ensure(2 * (ns / 8)); G.bb_sci.ensure(2 * (ns / 32));
-    G.exr_ci.ensure(ns / 4); G.gr_cj.ensure(ns / 8);
+    G.slotmap.ensure(ctx->natoms_global + 1);
+    NBX_CUDA(cudaMemsetAsync(G.slotmap.p, 0xff, sizeof(int) * (ctx->natoms_global + 1), st));
     NBX_CUDA(cudaMemsetAsync(G.f.p, 0, sizeof(float4) * ns, st));
     NBX_CUDA(cudaMemsetAsync(ctx->sumq2.p + g, 0, sizeof(double), st));
     if (G.nsci > 0) {
@@ -336,6 +312,7 @@ void grid_build(nbx_ctx* ctx, int g, int n, const float* x, const int* gid, cons
         S.type = G.type.p;
         S.xq = G.xq.p;
         S.wrapk = G.wrapk.p;
+        S.slotmap = G.slotmap.p;
         int threads = 128, blocks = (G.nsci * 32 + threads - 1) / threads;
         k_slab<<<blocks, threads, 0, st>>>(S);
         ctx->launches++;
@@ -345,13 +322,9 @@ void grid_build(nbx_ctx* ctx, int g, int n, const float* x, const int* gid, cons
         BA.order = G.order.p;
         BA.gid = G.gid.p;
         BA.xq = G.xq.p;
-        BA.excl_off = ctx->excl_off_g.p;
-        BA.excl_gid = ctx->excl_gid_g.p;
         BA.bb_ci = G.bb_ci.p;
         BA.bb_cj = G.bb_cj.p;
         BA.bb_sci = G.bb_sci.p;
-        BA.exr_ci = G.exr_ci.p;
-        BA.gr_cj = G.gr_cj.p;
         BA.sumq2 = ctx->sumq2.p;
         k_bbox<<<blocks, threads, 0, st>>>(BA, g);
         ctx->launches++;

@@ -1,18 +1,28 @@
 // search.cu -- cluster-pair search (KernelKind.PAIR_SEARCH, costs.py:32,163; pipeline.py:226-230)
 // and the rolling dynamic prune (KernelKind.PRUNE_ONLY, costs.py:31,162; pipeline.py:233-235).
 //
-// One warp per super-cluster.  Candidate j-clusters of one column are tested 32 per pass
-// (one per lane) against the shifted super-cluster and then the 8 i-cluster bounding boxes
-// at rlist_outer.  The list is written deterministically: a count pass, exclusive scans,
-// then a fill pass that writes every entry at its ballot/popc rank, so the output order is
-// the canonical (sci, shift, cj) order of the CPU oracle (ora_search) bit for bit.
-// The prune tests the 32 atom pairs of every active (i-cluster, j-cluster) tile at
-// rlist_inner with the current coordinates (one pair per lane, any() over the warp).
+// Search: one warp per super-cluster.  Per shift image, the warp enumerates the candidate
+// grid columns 32 at a time (one binary search over the column's z-sorted slabs per lane,
+// all in flight together), prefix-sums their j-cluster counts and then tests one candidate
+// j-cluster per lane: super-cluster bounding box, then the 8 i-cluster bounding boxes at
+// rlist_outer.  Exclusion masks are only computed for tiles that contain an excluded
+// partner (each i-atom's partners are mapped to their j-cluster through the grid's
+// gid -> slot map into a per-warp shared-memory list), contain filler slots, lie on the
+// diagonal, or belong to the nonlocal (global-id rule) list.  The list is written
+// deterministically: a count pass, exclusive scans, then a fill pass that writes every
+// entry at its ballot/popc rank -- the canonical (sci, shift, cj) order of the CPU oracle
+// (ora_search), bit for bit.
+//
+// Prune: one warp per sci entry, one cj entry per lane; every active tile tests its atom
+// pairs at rlist_inner and stops at the first hit; kept entries are compacted in order.
 #include <cub/device/device_scan.cuh>
 
 #include "nbx_internal.cuh"
 
 namespace nbx {
+
+constexpr int SEARCH_THREADS = 128;
+constexpr int EXMAX = 24; // partner j-clusters remembered per i-cluster (overflow -> always check)
 
 struct SearchArgs {
     // i grid
@@ -20,14 +30,13 @@ struct SearchArgs {
     const float4* bb_sci;
     const int* order_i;
     const int* gid_i;
-    const int2* exr_ci;
     int nsci_i;
     // j grid
     const float4* bb_cj;
     const float4* bb_sci_j;
     const int* order_j;
     const int* gid_j;
-    const int2* gr_cj;
+    const int* slotmap_j; // global id -> slot in grid j, or -1
     const int* col_start_j;
     int ncx_j, ncy_j;
     float lo_jx, lo_jy, inv_jx, inv_jy;
@@ -39,11 +48,16 @@ struct SearchArgs {
     int mode;
     float rl, rl2, rlm;
     // outputs
-    int* counts;        // [3][nsci]
+    int* counts;        // [3][nsci+1]
     const int* offsets; // [3][nsci+1]
     nbx_sci_entry* sci_out;
     nbx_cj_entry* cj_out;
     nbx_mask_pool_entry* pool_out;
+};
+
+struct WarpEx {
+    int cj[8][EXMAX];
+    int n[8];
 };
 
 __device__ __forceinline__ float bb_dist2(float4 alo, float4 ahi, float3 v, float4 blo, float4 bhi)
@@ -81,24 +95,31 @@ __device__ uint2 tile_masks(const SearchArgs& A, int ci, int cj, bool exov, bool
     return make_uint2(im, cm);
 }
 
+__device__ __forceinline__ bool has_partner(const WarpEx& X, int k, int cj)
+{
+    const int n = X.n[k];
+    if (n > EXMAX) return true;
+    bool hit = false;
+    for (int m = 0; m < n; m++) hit |= (X.cj[k][m] == cj);
+    return hit;
+}
+
 // Evaluate one candidate j-cluster; returns imask (bits 0-7) | need_pool (bit 8).
 // With `pool` non-null, also writes the 8 mask pairs of the entry.
-__device__ unsigned eval_candidate(const SearchArgs& A, int sci, int cj, float3 v, bool central,
-                                   float4 slo, float4 shi, nbx_mask_pool_entry* pool)
+__device__ unsigned eval_candidate(const SearchArgs& A, const WarpEx& X, int sci, int cj, float3 v,
+                                   bool central, float4 slo, float4 shi, nbx_mask_pool_entry* pool)
 {
     if (A.mode == NBX_LIST_LOCAL && central && cj < 4 * sci) return 0u;
     const float4 blo = A.bb_cj[2 * cj], bhi = A.bb_cj[2 * cj + 1];
     if (blo.w == 0.0f) return 0u;
     if (!(bb_dist2(slo, shi, v, blo, bhi) < A.rl2)) return 0u;
-    const int2 gr = A.gr_cj[cj];
     unsigned imask = 0u, need = 0u;
     for (int kk = 0; kk < 8; kk++) {
         const int ci = 8 * sci + kk;
         const float4 ilo = A.bb_ci[2 * ci], ihi = A.bb_ci[2 * ci + 1];
         uint2 m = make_uint2(0u, 0u);
         if (ilo.w != 0.0f && bb_dist2(ilo, ihi, v, blo, bhi) < A.rl2) {
-            const int2 er = A.exr_ci[ci];
-            const bool exov = !(er.y < gr.x || er.x > gr.y);
+            const bool exov = has_partner(X, kk, cj);
             const bool masked = ilo.w < 4.0f || blo.w < 8.0f || A.mode == NBX_LIST_NONLOCAL ||
                                 (central && (cj >> 2) == sci) || exov;
             m = make_uint2(0xffffffffu, 0u);
@@ -119,12 +140,34 @@ __device__ unsigned eval_candidate(const SearchArgs& A, int sci, int cj, float3 
 }
 
 template <bool FILL>
-__global__ void k_search(SearchArgs A)
+__global__ void __launch_bounds__(SEARCH_THREADS) k_search(SearchArgs A)
 {
+    __shared__ WarpEx s_ex[SEARCH_THREADS / 32];
     const int lane = threadIdx.x & 31;
     const int sci = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (sci >= A.nsci_i) return;
+    WarpEx& X = s_ex[threadIdx.x >> 5];
+    const unsigned FULL = 0xffffffffu;
     const unsigned lt = (1u << lane) - 1u;
+
+    // excluded partners of the 32 atoms -> their j-clusters in grid j, per i-cluster
+    if (lane < 8) X.n[lane] = 0;
+    __syncwarp();
+    {
+        const int slot = 32 * sci + lane;
+        if (A.order_i[slot] >= 0) {
+            const int g = A.gid_i[slot];
+            for (int e = A.excl_off[g]; e < A.excl_off[g + 1]; e++) {
+                const int sp = A.slotmap_j[A.excl_gid[e]];
+                if (sp >= 0) {
+                    const int pos = atomicAdd(&X.n[lane >> 2], 1);
+                    if (pos < EXMAX) X.cj[lane >> 2][pos] = sp >> 3;
+                }
+            }
+        }
+    }
+    __syncwarp();
+
     const float4 slo = A.bb_sci[2 * sci], shi = A.bb_sci[2 * sci + 1];
     int n_ent = 0, n_cj = 0, n_pool = 0;
     int ent_base = 0, cj_base = 0, pool_base = 0;
@@ -151,45 +194,68 @@ __global__ void k_search(SearchArgs A)
             cy0 = max(cy0, 0);
             cx1 = min(cx1, A.ncx_j - 1);
             cy1 = min(cy1, A.ncy_j - 1);
+            if (cx1 < cx0 || cy1 < cy0) continue;
             const float zlo = lz - A.rlm, zhi = hz + A.rlm;
+            const int nyr = cy1 - cy0 + 1;
+            const int ncols = (cx1 - cx0 + 1) * nyr;
             const int start_cj = n_cj;
-            for (int cx = cx0; cx <= cx1; cx++) {
-                for (int cy = cy0; cy <= cy1; cy++) {
-                    const int col = cx * A.ncy_j + cy;
+            for (int cb = 0; cb < ncols; cb += 32) {
+                // one column per lane: slab range by two binary searches (monotone z bounds)
+                const int ci_ = cb + lane;
+                int ks = 0, nc = 0;
+                if (ci_ < ncols) {
+                    const int col = (cx0 + ci_ / nyr) * A.ncy_j + (cy0 + ci_ % nyr);
                     const int k0 = A.col_start_j[col] >> 5, k1 = A.col_start_j[col + 1] >> 5;
-                    // first slab with hi.z >= zlo, first slab with lo.z > zhi (both monotone)
                     int a = k0, b = k1;
                     while (a < b) {
-                        int mid = (a + b) >> 1;
+                        const int mid = (a + b) >> 1;
                         if (A.bb_sci_j[2 * mid + 1].z < zlo) a = mid + 1; else b = mid;
                     }
-                    const int ks = a;
+                    ks = a;
                     b = k1;
                     while (a < b) {
-                        int mid = (a + b) >> 1;
+                        const int mid = (a + b) >> 1;
                         if (A.bb_sci_j[2 * mid].z > zhi) b = mid; else a = mid + 1;
                     }
-                    const int ke = a;
-                    for (int c0 = 4 * ks; c0 < 4 * ke; c0 += 32) {
-                        const int cj = c0 + lane;
-                        unsigned res = 0u;
-                        if (cj < 4 * ke) res = eval_candidate(A, sci, cj, v, central, slo, shi, nullptr);
-                        const unsigned has = __ballot_sync(0xffffffffu, (res & 0xffu) != 0u);
-                        const unsigned pb = __ballot_sync(0xffffffffu, (res >> 8) != 0u);
-                        if (FILL && (res & 0xffu)) {
-                            unsigned pidx = 0u;
-                            if (res >> 8) {
-                                pidx = (unsigned)(pool_base + n_pool + __popc(pb & lt));
-                                eval_candidate(A, sci, cj, v, central, slo, shi, A.pool_out + pidx);
-                            }
-                            nbx_cj_entry e;
-                            e.cj = cj;
-                            e.meta = (res & 0xffu) | (pidx << 8);
-                            A.cj_out[cj_base + n_cj + __popc(has & lt)] = e;
-                        }
-                        n_cj += __popc(has);
-                        n_pool += __popc(pb);
+                    nc = 4 * (a - ks);
+                }
+                int incl = nc;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int t = __shfl_up_sync(FULL, incl, o);
+                    if (lane >= o) incl += t;
+                }
+                const int excl = incl - nc;
+                const int total = __shfl_sync(FULL, incl, 31);
+                for (int tb = 0; tb < total; tb += 32) {
+                    const int t = tb + lane;
+                    int own = 0;
+#pragma unroll
+                    for (int st = 16; st > 0; st >>= 1) {
+                        const int c = own + st;
+                        const int ec = __shfl_sync(FULL, excl, c & 31);
+                        if (c < 32 && ec <= t) own = c;
                     }
+                    const int base_o = __shfl_sync(FULL, excl, own);
+                    const int ks_o = __shfl_sync(FULL, ks, own);
+                    const int cj = 4 * ks_o + (t - base_o);
+                    unsigned res = 0u;
+                    if (t < total) res = eval_candidate(A, X, sci, cj, v, central, slo, shi, nullptr);
+                    const unsigned has = __ballot_sync(FULL, (res & 0xffu) != 0u);
+                    const unsigned pb = __ballot_sync(FULL, (res >> 8) != 0u);
+                    if (FILL && (res & 0xffu)) {
+                        unsigned pidx = 0u;
+                        if (res >> 8) {
+                            pidx = (unsigned)(pool_base + n_pool + __popc(pb & lt));
+                            eval_candidate(A, X, sci, cj, v, central, slo, shi, A.pool_out + pidx);
+                        }
+                        nbx_cj_entry e;
+                        e.cj = cj;
+                        e.meta = (res & 0xffu) | (pidx << 8);
+                        A.cj_out[cj_base + n_cj + __popc(has & lt)] = e;
+                    }
+                    n_cj += __popc(has);
+                    n_pool += __popc(pb);
                 }
             }
             if (n_cj > start_cj) {
@@ -232,8 +298,11 @@ struct PruneArgs {
     nbx_cj_entry* cj_in;
 };
 
-__global__ void __launch_bounds__(256) k_prune(PruneArgs A)
+constexpr int PRUNE_THREADS = 256;
+
+__global__ void __launch_bounds__(PRUNE_THREADS) k_prune(PruneArgs A)
 {
+    __shared__ float4 s_xi[PRUNE_THREADS];
     const int lane = threadIdx.x & 31;
     const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int e = A.part + A.nparts * w;
@@ -241,47 +310,49 @@ __global__ void __launch_bounds__(256) k_prune(PruneArgs A)
     const unsigned lt = (1u << lane) - 1u;
     const nbx_sci_entry se = A.sci[e];
     const float3 v = shift_vec(se.shift, A.box);
-    const int i = lane >> 3, j = lane & 7;
-    float3 xi[8];
-#pragma unroll
-    for (int kk = 0; kk < 8; kk++) {
-        float4 t = A.xq_i[32 * se.sci + 4 * kk + i];
-        xi[kk] = make_float3(__fadd_rn(t.x, v.x), __fadd_rn(t.y, v.y), __fadd_rn(t.z, v.z));
+    float4* xi = s_xi + (threadIdx.x & ~31);
+    {
+        const float4 t = A.xq_i[32 * se.sci + lane];
+        xi[lane] = make_float4(__fadd_rn(t.x, v.x), __fadd_rn(t.y, v.y), __fadd_rn(t.z, v.z), 0.f);
     }
+    __syncwarp();
     int kept = 0;
     for (int c0 = se.cj_start; c0 < se.cj_end; c0 += 32) {
+        const int q = c0 + lane;
         nbx_cj_entry my;
         my.cj = 0;
         my.meta = 0u;
-        if (c0 + lane < se.cj_end) my = A.cj[c0 + lane];
-        const int nb = min(32, se.cj_end - c0);
-        unsigned mynew = 0u;
-        for (int t = 0; t < nb; t++) {
-            const int cj = __shfl_sync(0xffffffffu, my.cj, t);
-            const unsigned meta = __shfl_sync(0xffffffffu, my.meta, t);
-            const unsigned imask = meta & 0xffu, pidx = meta >> 8;
-            const float4 xj = A.xq_j[8 * cj + j];
-            unsigned nm = 0u;
+        if (q < se.cj_end) my = A.cj[q];
+        unsigned nm = 0u;
+        const unsigned imask = my.meta & 0xffu, pidx = my.meta >> 8;
+        if (imask) {
+            float4 xj[8];
 #pragma unroll
+            for (int j = 0; j < 8; j++) xj[j] = A.xq_j[8 * my.cj + j];
             for (int kk = 0; kk < 8; kk++) {
-                if (imask & (1u << kk)) {
-                    unsigned pm = 0xffffffffu;
-                    if (pidx) pm = A.pool[pidx].m[kk][0] | A.pool[pidx].m[kk][1];
-                    const float dx = __fsub_rn(xi[kk].x, xj.x);
-                    const float dy = __fsub_rn(xi[kk].y, xj.y);
-                    const float dz = __fsub_rn(xi[kk].z, xj.z);
-                    const float r2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
-                    const bool hit = ((pm >> lane) & 1u) && (r2 < A.rli2);
-                    if (__any_sync(0xffffffffu, hit)) nm |= 1u << kk;
+                if (!(imask & (1u << kk))) continue;
+                unsigned pm = 0xffffffffu;
+                if (pidx) pm = A.pool[pidx].m[kk][0] | A.pool[pidx].m[kk][1];
+                bool hit = false;
+                for (int i = 0; i < 4 && !hit; i++) {
+                    const float4 a = xi[4 * kk + i];
+#pragma unroll
+                    for (int j = 0; j < 8; j++) {
+                        const float dx = __fsub_rn(a.x, xj[j].x);
+                        const float dy = __fsub_rn(a.y, xj[j].y);
+                        const float dz = __fsub_rn(a.z, xj[j].z);
+                        const float r2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
+                        hit |= ((pm >> (i * 8 + j)) & 1u) && (r2 < A.rli2);
+                    }
                 }
+                if (hit) nm |= 1u << kk;
             }
-            if (lane == t) mynew = nm;
         }
-        const unsigned keep = __ballot_sync(0xffffffffu, mynew != 0u);
-        if (mynew) {
+        const unsigned keep = __ballot_sync(0xffffffffu, nm != 0u);
+        if (nm) {
             nbx_cj_entry o;
             o.cj = my.cj;
-            o.meta = mynew | (my.meta & ~0xffu);
+            o.meta = nm | (my.meta & ~0xffu);
             A.cj_in[se.cj_start + kept + __popc(keep & lt)] = o;
         }
         kept += __popc(keep);
@@ -326,13 +397,8 @@ __global__ void __launch_bounds__(256) k_count_pairs(PruneArgs A, float rc2, uns
     }
 }
 
-void count_pairs(nbx_ctx* ctx, int l, long long* pairs, long long* slots, cudaStream_t st)
+static PruneArgs prune_args(nbx_ctx* ctx, List& L)
 {
-    List& L = ctx->list[l];
-    if (!L.built) throw CudaError{cudaErrorInvalidValue, "count before search"};
-    *pairs = 0;
-    *slots = 0;
-    if (L.n_sci == 0) return;
     PruneArgs A;
     A.sci = L.sci.p;
     A.n_sci = (int)L.n_sci;
@@ -346,6 +412,17 @@ void count_pairs(nbx_ctx* ctx, int l, long long* pairs, long long* slots, cudaSt
     A.rli2 = ctx->c.rli2;
     A.sci_in = L.sci_in.p;
     A.cj_in = L.cj_in.p;
+    return A;
+}
+
+void count_pairs(nbx_ctx* ctx, int l, long long* pairs, long long* slots, cudaStream_t st)
+{
+    List& L = ctx->list[l];
+    if (!L.built) throw CudaError{cudaErrorInvalidValue, "count before search"};
+    *pairs = 0;
+    *slots = 0;
+    if (L.n_sci == 0) return;
+    PruneArgs A = prune_args(ctx, L);
     DBuf<unsigned long long> out;
     out.ensure(2);
     NBX_CUDA(cudaMemsetAsync(out.p, 0, 2 * sizeof(unsigned long long), st));
@@ -365,23 +442,12 @@ void prune(nbx_ctx* ctx, int l, int part, int nparts, cudaStream_t st)
     List& L = ctx->list[l];
     if (!L.built) throw CudaError{cudaErrorInvalidValue, "prune before search"};
     if (L.n_sci == 0) return;
-    PruneArgs A;
-    A.sci = L.sci.p;
-    A.n_sci = (int)L.n_sci;
+    PruneArgs A = prune_args(ctx, L);
     A.part = part;
     A.nparts = nparts;
-    A.cj = L.cj.p;
-    A.pool = L.pool.p;
-    A.xq_i = ctx->grid[L.gi].xq.p;
-    A.xq_j = ctx->grid[L.gj].xq.p;
-    A.box = make_float3(ctx->box[0], ctx->box[1], ctx->box[2]);
-    A.rli2 = ctx->c.rli2;
-    A.sci_in = L.sci_in.p;
-    A.cj_in = L.cj_in.p;
     const int nw = (int)((L.n_sci - part + nparts - 1) / nparts);
     if (nw <= 0) return;
-    const int threads = 256;
-    k_prune<<<(nw * 32 + threads - 1) / threads, threads, 0, st>>>(A);
+    k_prune<<<(nw * 32 + PRUNE_THREADS - 1) / PRUNE_THREADS, PRUNE_THREADS, 0, st>>>(A);
     ctx->launches++;
     NBX_CUDA(cudaGetLastError());
 }
@@ -401,13 +467,12 @@ void search(nbx_ctx* ctx, int l, cudaStream_t st)
     A.bb_sci = GI.bb_sci.p;
     A.order_i = GI.order.p;
     A.gid_i = GI.gid.p;
-    A.exr_ci = GI.exr_ci.p;
     A.nsci_i = nsci;
     A.bb_cj = GJ.bb_cj.p;
     A.bb_sci_j = GJ.bb_sci.p;
     A.order_j = GJ.order.p;
     A.gid_j = GJ.gid.p;
-    A.gr_cj = GJ.gr_cj.p;
+    A.slotmap_j = GJ.slotmap.p;
     A.col_start_j = GJ.col_start.p;
     A.ncx_j = GJ.ncx;
     A.ncy_j = GJ.ncy;
@@ -432,10 +497,9 @@ void search(nbx_ctx* ctx, int l, cudaStream_t st)
     NBX_CUDA(cudaMemsetAsync(L.counts.p, 0, sizeof(int) * n3, st));
     A.counts = L.counts.p;
     A.offsets = L.offsets.p;
-    const int threads = 128;
-    const int blocks = (nsci * 32 + threads - 1) / threads;
+    const int blocks = (nsci * 32 + SEARCH_THREADS - 1) / SEARCH_THREADS;
     if (nsci > 0) {
-        k_search<false><<<blocks, threads, 0, st>>>(A);
+        k_search<false><<<blocks, SEARCH_THREADS, 0, st>>>(A);
         ctx->launches++;
         NBX_CUDA(cudaGetLastError());
     }
@@ -467,7 +531,7 @@ void search(nbx_ctx* ctx, int l, cudaStream_t st)
     k_pool0<<<1, 32, 0, st>>>(L.pool.p);
     ctx->launches++;
     if (nsci > 0) {
-        k_search<true><<<blocks, threads, 0, st>>>(A);
+        k_search<true><<<blocks, SEARCH_THREADS, 0, st>>>(A);
         ctx->launches++;
         NBX_CUDA(cudaGetLastError());
     }
