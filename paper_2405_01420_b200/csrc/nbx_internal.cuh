@@ -81,7 +81,7 @@ struct List {
 };
 
 struct ForceConsts {
-    float epsfac, k_rf, two_k_rf, c_rf, beta, beta2, beta3, sh_ewald, sh_lj6, sh_lj12, rc2, rli2;
+    float epsfac, k_rf, two_k_rf, c_rf, beta, beta2, beta3, beta3_monic, sh_ewald, sh_lj6, sh_lj12, rc2, rli2;
 };
 
 } // namespace nbx

@@ -334,15 +334,31 @@ __global__ void __launch_bounds__(PRUNE_THREADS) k_prune(PruneArgs A)
                 unsigned pm = 0xffffffffu;
                 if (pidx) pm = A.pool[pidx].m[kk][0] | A.pool[pidx].m[kk][1];
                 bool hit = false;
-                for (int i = 0; i < 4 && !hit; i++) {
-                    const float4 a = xi[4 * kk + i];
+                if (pm == 0xffffffffu) {
+                    // unmasked tile (the common case): no per-pair mask bits to test
+                    for (int i = 0; i < 4 && !hit; i++) {
+                        const float4 a = xi[4 * kk + i];
 #pragma unroll
-                    for (int j = 0; j < 8; j++) {
-                        const float dx = __fsub_rn(a.x, xj[j].x);
-                        const float dy = __fsub_rn(a.y, xj[j].y);
-                        const float dz = __fsub_rn(a.z, xj[j].z);
-                        const float r2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
-                        hit |= ((pm >> (i * 8 + j)) & 1u) && (r2 < A.rli2);
+                        for (int j = 0; j < 8; j++) {
+                            const float dx = __fsub_rn(a.x, xj[j].x);
+                            const float dy = __fsub_rn(a.y, xj[j].y);
+                            const float dz = __fsub_rn(a.z, xj[j].z);
+                            hit |= __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx))) < A.rli2;
+                        }
+                    }
+                } else {
+                    for (int i = 0; i < 4 && !hit; i++) {
+                        const unsigned row = (pm >> (i * 8)) & 0xffu;
+                        if (!row) continue;
+                        const float4 a = xi[4 * kk + i];
+#pragma unroll
+                        for (int j = 0; j < 8; j++) {
+                            const float dx = __fsub_rn(a.x, xj[j].x);
+                            const float dy = __fsub_rn(a.y, xj[j].y);
+                            const float dz = __fsub_rn(a.z, xj[j].z);
+                            const float r2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
+                            hit |= ((row >> j) & 1u) && (r2 < A.rli2);
+                        }
                     }
                 }
                 if (hit) nm |= 1u << kk;

@@ -19,7 +19,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libnbx.so")
+LIB_PATH = os.environ.get("NBX_LIB") or os.path.join(HERE, "libnbx.so")  # NBX_LIB: variant builds (tools/)
 
 NBX_COULOMB_RF, NBX_COULOMB_EWALD = 0, 1
 LIST_LOCAL, LIST_NONLOCAL = 0, 1

@@ -1,0 +1,75 @@
+"""Build force-kernel variants (-D flags) and time them on a GPU.
+
+    python tools/force_variants.py build            # here (nvcc cross-compile)
+    python tools/force_variants.py run [config]     # on the GPU box
+"""
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+OUT = os.path.join(ROOT, "scratch", "variants")
+VARIANTS = {
+    "base": [],
+    "t192b3": ["-DNBX_FORCE_THREADS=192", "-DNBX_FORCE_MINB=3"],
+    "t160b4": ["-DNBX_FORCE_THREADS=160", "-DNBX_FORCE_MINB=4"],
+    "t128b4": ["-DNBX_FORCE_THREADS=128", "-DNBX_FORCE_MINB=4"],
+    "t96b5": ["-DNBX_FORCE_THREADS=96", "-DNBX_FORCE_MINB=5"],
+}
+
+
+def build():
+    sys.path.insert(0, ROOT)
+    from paper_2405_01420_b200 import build as B
+    os.makedirs(OUT, exist_ok=True)
+    for name, flags in VARIANTS.items():
+        objs = []
+        for src in B.SOURCES:
+            o = os.path.join(OUT, f"{name}_{src}.o")
+            extra = B.PER_FILE.get(src, [])
+            cmd = [B._nvcc(), *B.ARCH, *B.NVCC_FLAGS, *extra, *flags, "-c", os.path.join(B.CSRC, src), "-o", o]
+            subprocess.check_call(cmd, stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+            objs.append(o)
+        subprocess.check_call([B._nvcc(), *B.ARCH, "-shared", "-o", os.path.join(OUT, f"libnbx_{name}.so"), *objs,
+                               "-lcudart"])
+        print("built", name)
+
+
+def run_one(name, cfg, reps=20):
+    os.environ["NBX_LIB"] = os.path.join(OUT, f"libnbx_{name}.so")
+    sys.path.insert(0, ROOT)
+    import torch
+    from paper_2405_01420_b200 import nbx, systems
+    s = systems.make(cfg)
+    nb = nbx.Nonbonded(s)
+    x = torch.from_numpy(s.x).cuda()
+    f = torch.empty_like(x)
+    nb.search(x)
+    nb.forces(x, out=f)
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(st)
+    for _ in range(reps):
+        nb.compute()
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    nb.get_f(f)
+    p, sl = nb.count_pairs()
+    return {"variant": name, "config": cfg, "force_ms": ms, "slot_tflops": sl * 57 / ms / 1e9,
+            "pairs_per_s": p / ms * 1e3}
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "build":
+        build()
+    elif sys.argv[1] == "run":
+        cfg = sys.argv[2] if len(sys.argv) > 2 else "stmv"
+        names = sys.argv[3].split(",") if len(sys.argv) > 3 else list(VARIANTS)
+        for n in names:
+            r = subprocess.run([sys.executable, __file__, "one", cfg, n], capture_output=True, text=True)
+            print(r.stdout.strip().splitlines()[-1] if r.stdout.strip() else r.stderr[-500:], flush=True)
+    elif sys.argv[1] == "one":
+        print(json.dumps(run_one(sys.argv[3], sys.argv[2])))
