@@ -314,7 +314,8 @@ class DomainDecomposition:
             eng.halo_unpack_add(self.f_ext, p.up_idx, self.fbuf_up[k])
 
     def step(self, x_home=None, step=1, energy=False, virial=False, prune=None):
-        """One NB-path step (non-search): returns f_home view (and energies/virial if asked)."""
+        """One NB-path step: returns f_home (a view of the rank's force buffer, overwritten by
+        the next step) and, with energy/virial, the all-reduced (energies, virial)."""
         eng = self.engine
         if x_home is not None:
             self.x_ext[:self.n_home].copy_(x_home)

@@ -27,6 +27,7 @@ def main():
     xg = torch.from_numpy(s.x).to(dev)
     d.repartition(xg)
     f, (e, vir) = d.step(None, step=1, energy=True, virial=True, prune=False)
+    f = f.clone()  # step() returns a view of the rank's force buffer
     # a second, non-search step with moved atoms (halo coordinates refreshed, prune on)
     rng = np.random.default_rng(3)
     disp = torch.from_numpy(rng.uniform(-0.01, 0.01, size=s.x.shape).astype(np.float32)).to(dev)

@@ -12,10 +12,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "scratch", "variants")
 VARIANTS = {
     "base": [],
-    "t192b3": ["-DNBX_FORCE_THREADS=192", "-DNBX_FORCE_MINB=3"],
-    "t160b4": ["-DNBX_FORCE_THREADS=160", "-DNBX_FORCE_MINB=4"],
-    "t128b4": ["-DNBX_FORCE_THREADS=128", "-DNBX_FORCE_MINB=4"],
-    "t96b5": ["-DNBX_FORCE_THREADS=96", "-DNBX_FORCE_MINB=5"],
+    "pair": ["-DNBX_PAIRTILE=1"],
+    "pair_t160b4": ["-DNBX_PAIRTILE=1", "-DNBX_FORCE_THREADS=160", "-DNBX_FORCE_MINB=4"],
 }
 
 
