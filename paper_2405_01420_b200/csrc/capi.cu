@@ -145,7 +145,7 @@ NBX_API int nbx_destroy(nbx_ctx* ctx)
         G.key.release(); G.key_out.release(); G.val.release(); G.val_out.release(); G.xw.release();
         G.order.release(); G.gid.release(); G.type.release(); G.xq.release(); G.wrapk.release();
         G.f.release(); G.bb_ci.release(); G.bb_cj.release(); G.bb_sci.release();
-        G.slotmap.release(); G.tmp.release();
+        G.slotmap.release(); G.bb_col.release(); G.tmp.release();
         List& L = ctx->list[g];
         L.sci.release(); L.sci_in.release(); L.cj.release(); L.cj_in.release(); L.pool.release();
         L.counts.release(); L.offsets.release(); L.totals.release(); L.tmp.release();

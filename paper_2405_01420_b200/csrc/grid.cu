@@ -207,6 +207,24 @@ __global__ void k_bbox(BBArgs A, int gslot)
     }
 }
 
+// x-y bounding box of every column (union of its slab boxes), for the search's exact
+// column pre-test; empty columns get an empty box
+__global__ void k_colbox(int ncol, const int* __restrict__ col_start, const float4* __restrict__ bb_sci,
+                         float4* __restrict__ bb_col)
+{
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= ncol) return;
+    float4 b = make_float4(NBX_BB_EMPTY, NBX_BB_EMPTY, -NBX_BB_EMPTY, -NBX_BB_EMPTY);
+    for (int k = col_start[c] >> 5; k < (col_start[c + 1] >> 5); k++) {
+        const float4 lo = bb_sci[2 * k], hi = bb_sci[2 * k + 1];
+        b.x = fminf(b.x, lo.x);
+        b.y = fminf(b.y, lo.y);
+        b.z = fmaxf(b.z, hi.x);
+        b.w = fmaxf(b.w, hi.y);
+    }
+    bb_col[c] = b;
+}
+
 // host-side grid dimensions: the same formula as ora_grid_dims (oracle/nbx_oracle.c)
 static void grid_dims(const float size[3], double density, int* ncx, int* ncy, float inv_cell[2])
 {
@@ -330,6 +348,10 @@ void grid_build(nbx_ctx* ctx, int g, int n, const float* x, const int* gid, cons
         ctx->launches++;
         NBX_CUDA(cudaGetLastError());
     }
+    G.bb_col.ensure(G.ncol);
+    k_colbox<<<(G.ncol + 255) / 256, 256, 0, st>>>(G.ncol, G.col_start.p, G.bb_sci.p, G.bb_col.p);
+    ctx->launches++;
+    NBX_CUDA(cudaGetLastError());
     G.built = true;
 }
 

@@ -63,6 +63,7 @@ struct Grid {
     DBuf<float4> wrapk;                         // [nslots] kx,ky,kz,q
     DBuf<float4> f;                             // [nslots] cluster forces (w unused)
     DBuf<float4> bb_ci, bb_cj, bb_sci;          // 2 float4 per cluster: lo (w = nreal), hi
+    DBuf<float4> bb_col;                        // per column: (xlo, ylo, xhi, yhi) of its atoms
     DBuf<int> slotmap;                          // global id -> slot, or -1 [natoms_global]
     DBuf<char> tmp;                             // cub temp
 };

@@ -38,6 +38,7 @@ struct SearchArgs {
     const int* gid_j;
     const int* slotmap_j; // global id -> slot in grid j, or -1
     const int* col_start_j;
+    const float4* bb_col_j; // (xlo, ylo, xhi, yhi) per column
     int ncx_j, ncy_j;
     float lo_jx, lo_jy, inv_jx, inv_jy;
     // topology
@@ -203,8 +204,17 @@ __global__ void __launch_bounds__(SEARCH_THREADS) k_search(SearchArgs A)
                 // one column per lane: slab range by two binary searches (monotone z bounds)
                 const int ci_ = cb + lane;
                 int ks = 0, nc = 0;
+                int col = -1;
                 if (ci_ < ncols) {
-                    const int col = (cx0 + ci_ / nyr) * A.ncy_j + (cy0 + ci_ % nyr);
+                    col = (cx0 + ci_ / nyr) * A.ncy_j + (cy0 + ci_ % nyr);
+                    // exact pre-test: every j-cluster of the column lies inside the column's x-y
+                    // box, and fp add/sub/max/fma are monotone, so d2(column) <= d2(any cj)
+                    const float4 cb_ = A.bb_col_j[col];
+                    const float ddx = fmaxf(0.0f, fmaxf(__fsub_rn(lx, cb_.z), __fsub_rn(cb_.x, hx)));
+                    const float ddy = fmaxf(0.0f, fmaxf(__fsub_rn(ly, cb_.w), __fsub_rn(cb_.y, hy)));
+                    if (!(__fmaf_rn(ddy, ddy, __fmul_rn(ddx, ddx)) < A.rl2)) col = -1;
+                }
+                if (col >= 0) {
                     const int k0 = A.col_start_j[col] >> 5, k1 = A.col_start_j[col + 1] >> 5;
                     int a = k0, b = k1;
                     while (a < b) {
@@ -490,6 +500,7 @@ void search(nbx_ctx* ctx, int l, cudaStream_t st)
     A.gid_j = GJ.gid.p;
     A.slotmap_j = GJ.slotmap.p;
     A.col_start_j = GJ.col_start.p;
+    A.bb_col_j = GJ.bb_col.p;
     A.ncx_j = GJ.ncx;
     A.ncy_j = GJ.ncy;
     A.lo_jx = GJ.lo[0];

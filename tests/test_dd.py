@@ -79,7 +79,7 @@ def _worker(rank, world, port, outdir):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_dd_matches_single_domain(world):
     from oracle import oracle as O
     s = _system()
