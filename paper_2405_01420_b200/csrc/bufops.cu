@@ -3,7 +3,7 @@
 //  put_x   X buffer op (folded into NBNXM_* in the reference model, pipeline.py:231):
 //          cluster-ordered xyzq from user-order x with the search-time wrap shifts.
 //  get_f   F buffer op, KernelKind.REDUCE_FORCES (costs.py:41,172; pipeline.py:250-254,398-401):
-//          cluster forces -> user order, read-and-clear so no memset is needed next step.
+//          cluster forces -> user order (gather by input atom), then the cluster buffer is cleared.
 //  halo    KernelKind.HALO_PACK_UNPACK (costs.py:43,174; pipeline.py:366-379, 406-417).
 // All of these are HBM/L2-bandwidth bound gathers/scatters: one thread per slot, float4
 // accesses on the cluster side.
@@ -24,15 +24,14 @@ __global__ void k_put_x(int nslots, const int* __restrict__ order, const float4*
                         __fmaf_rn(-k.z, box.z, x2), k.w);
 }
 
-__global__ void k_get_f(int nslots, const int* __restrict__ order, float4* __restrict__ fc,
+// gather form: one thread per input atom, coalesced 12-byte writes of f, one 16-byte read of
+// its cluster slot; the cluster buffer is cleared afterwards with a memset
+__global__ void k_get_f(int n, const int* __restrict__ islot, const float4* __restrict__ fc,
                         float* __restrict__ f, int accumulate)
 {
-    int s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= nslots) return;
-    int a = order[s];
-    float4 v = fc[s];
-    fc[s] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (a < 0) return;
+    const int a = blockIdx.x * blockDim.x + threadIdx.x;
+    if (a >= n) return;
+    const float4 v = fc[islot[a]];
     if (accumulate) {
         f[3 * a] += v.x;
         f[3 * a + 1] += v.y;
@@ -110,9 +109,12 @@ void get_f(nbx_ctx* ctx, int g, float* f, int accumulate, cudaStream_t st)
     Grid& G = ctx->grid[g];
     if (!G.built) throw CudaError{cudaErrorInvalidValue, "get_f before grid build"};
     if (G.nslots == 0) return;
-    k_get_f<<<(G.nslots + 255) / 256, 256, 0, st>>>(G.nslots, G.order.p, G.f.p, f, accumulate);
-    ctx->launches++;
-    NBX_CUDA(cudaGetLastError());
+    if (G.n > 0) {
+        k_get_f<<<(G.n + 255) / 256, 256, 0, st>>>(G.n, G.islot.p, G.f.p, f, accumulate);
+        ctx->launches++;
+        NBX_CUDA(cudaGetLastError());
+    }
+    NBX_CUDA(cudaMemsetAsync(G.f.p, 0, sizeof(float4) * G.nslots, st));
 }
 
 void virial_sum(nbx_ctx* ctx, int g, cudaStream_t st)

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -128,6 +129,10 @@ NBX_API int nbx_create(int device, const nbx_params* p, nbx_ctx** out)
     ctx->sumq2.ensure(2);
     NBX_CUDA(cudaMemset(ctx->sumq2.p, 0, sizeof(double) * 2));
     ctx->counter.ensure(8);
+    // Row f2 (list sorting by length) is available but off by default: on the
+    // 12M box the longest-first order costs L2 locality (force kernel +6%), and the tail it
+    // removes is ~3% (ncu sm__cycles_active min/max) -- see DESIGN.md section 5
+    if (const char* eo = std::getenv("NBX_ENTRY_ORDER")) ctx->entry_order = std::atoi(eo);
     *out = ctx;
     return NBX_OK;
     NBX_GUARD_END
@@ -145,10 +150,12 @@ NBX_API int nbx_destroy(nbx_ctx* ctx)
         G.key.release(); G.key_out.release(); G.val.release(); G.val_out.release(); G.xw.release();
         G.order.release(); G.gid.release(); G.type.release(); G.xq.release(); G.wrapk.release();
         G.f.release(); G.bb_ci.release(); G.bb_cj.release(); G.bb_sci.release();
-        G.slotmap.release(); G.bb_col.release(); G.tmp.release();
+        G.slotmap.release(); G.islot.release(); G.bb_col.release(); G.tmp.release();
         List& L = ctx->list[g];
         L.sci.release(); L.sci_in.release(); L.cj.release(); L.cj_in.release(); L.pool.release();
         L.counts.release(); L.offsets.release(); L.totals.release(); L.tmp.release();
+        L.len_key.release(); L.len_key_out.release(); L.order_in.release(); L.order.release(); L.sort_tmp.release();
+        L.flags.release(); L.tsci.release(); L.tcj.release(); L.tpool.release();
     }
     ctx->q_g.release(); ctx->type_g.release(); ctx->excl_off_g.release(); ctx->excl_gid_g.release();
     ctx->c6c12s.release(); ctx->acc.release(); ctx->sumq2.release(); ctx->counter.release();

@@ -82,6 +82,7 @@ struct SlabArgs {
     float4* xq;
     float4* wrapk;
     int* slotmap;
+    int* islot;
 };
 
 // rank of this lane's key among the real lanes of the same group (ties impossible: idx)
@@ -139,6 +140,7 @@ __global__ void k_slab(SlabArgs A)
         A.xq[slot] = make_float4(w.x, w.y, w.z, q);
         A.wrapk[slot] = make_float4(k.x, k.y, k.z, q);
         A.slotmap[g] = slot;
+        A.islot[idx] = slot;
     }
     if (!((occ >> lane) & 1u)) {
         int slot = slot0 + lane;
@@ -310,6 +312,7 @@ void grid_build(nbx_ctx* ctx, int g, int n, const float* x, const int* gid, cons
     G.xq.ensure(ns); G.wrapk.ensure(ns); G.f.ensure(ns);
     G.bb_ci.ensure(2 * (ns / 4)); G.bb_cj.ensure(2 * (ns / 8)); G.bb_sci.ensure(2 * (ns / 32));
     G.slotmap.ensure(ctx->natoms_global + 1);
+    G.islot.ensure(nn);
     NBX_CUDA(cudaMemsetAsync(G.slotmap.p, 0xff, sizeof(int) * (ctx->natoms_global + 1), st));
     NBX_CUDA(cudaMemsetAsync(G.f.p, 0, sizeof(float4) * ns, st));
     NBX_CUDA(cudaMemsetAsync(ctx->sumq2.p + g, 0, sizeof(double), st));
@@ -331,6 +334,7 @@ void grid_build(nbx_ctx* ctx, int g, int n, const float* x, const int* gid, cons
         S.xq = G.xq.p;
         S.wrapk = G.wrapk.p;
         S.slotmap = G.slotmap.p;
+        S.islot = G.islot.p;
         int threads = 128, blocks = (G.nsci * 32 + threads - 1) / threads;
         k_slab<<<blocks, threads, 0, st>>>(S);
         ctx->launches++;

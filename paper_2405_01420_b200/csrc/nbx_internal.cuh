@@ -65,6 +65,7 @@ struct Grid {
     DBuf<float4> bb_ci, bb_cj, bb_sci;          // 2 float4 per cluster: lo (w = nreal), hi
     DBuf<float4> bb_col;                        // per column: (xlo, ylo, xhi, yhi) of its atoms
     DBuf<int> slotmap;                          // global id -> slot, or -1 [natoms_global]
+    DBuf<int> islot;                            // input index -> slot [n]
     DBuf<char> tmp;                             // cub temp
 };
 
@@ -78,6 +79,14 @@ struct List {
     DBuf<int> counts;  // [3][nsci+1]
     DBuf<int> offsets; // [3][nsci+1]
     DBuf<int> totals;  // [3]
+    DBuf<unsigned> len_key, len_key_out;        // force-kernel work order (row f2)
+    DBuf<int> order_in, order;                  // sci entries, longest first
+    DBuf<char> sort_tmp;
+    DBuf<int> flags;                            // search overflow / max counts
+    int cap_cj = 0, cap_pool = 0;               // single-pass per-sci capacities
+    DBuf<nbx_sci_entry> tsci;                   // single-pass private outputs
+    DBuf<nbx_cj_entry> tcj;
+    DBuf<nbx_mask_pool_entry> tpool;
     DBuf<char> tmp;
 };
 
@@ -107,6 +116,7 @@ struct nbx_ctx {
     nbx::DBuf<double> sumq2;  // [2] per grid
     nbx::DBuf<int> counter;   // work counters [8]
     int64_t launches = 0;
+    int entry_order = 0; // 0: list order (spatially coherent), 1: longest first (env NBX_ENTRY_ORDER)
 };
 
 namespace nbx {

@@ -15,6 +15,7 @@
 //
 // Prune: one warp per sci entry, one cj entry per lane; every active tile tests its atom
 // pairs at rlist_inner and stops at the first hit; kept entries are compacted in order.
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include "nbx_internal.cuh"
@@ -54,11 +55,17 @@ struct SearchArgs {
     nbx_sci_entry* sci_out;
     nbx_cj_entry* cj_out;
     nbx_mask_pool_entry* pool_out;
+    // single pass: per-sci private regions of capacity cap_cj / cap_pool, compacted afterwards
+    int cap_cj, cap_pool;
+    int* flags; // [0] overflow, [1] max n_cj per sci, [2] max n_pool per sci
 };
+
+enum { SEARCH_COUNT = 0, SEARCH_FILL = 1, SEARCH_SINGLE = 2 };
 
 struct WarpEx {
     int cj[8][EXMAX];
     int n[8];
+    int surv[32]; // candidates that passed the super-cluster test, in candidate order
 };
 
 __device__ __forceinline__ float bb_dist2(float4 alo, float4 ahi, float3 v, float4 blo, float4 bhi)
@@ -105,42 +112,35 @@ __device__ __forceinline__ bool has_partner(const WarpEx& X, int k, int cj)
     return hit;
 }
 
-// Evaluate one candidate j-cluster; returns imask (bits 0-7) | need_pool (bit 8).
-// With `pool` non-null, also writes the 8 mask pairs of the entry.
-__device__ unsigned eval_candidate(const SearchArgs& A, const WarpEx& X, int sci, int cj, float3 v,
-                                   bool central, float4 slo, float4 shi, nbx_mask_pool_entry* pool)
+// super-cluster level test of one candidate j-cluster
+__device__ __forceinline__ bool sci_test(const SearchArgs& A, int sci, int cj, float3 v, bool central,
+                                         float4 slo, float4 shi)
 {
-    if (A.mode == NBX_LIST_LOCAL && central && cj < 4 * sci) return 0u;
+    if (A.mode == NBX_LIST_LOCAL && central && cj < 4 * sci) return false;
     const float4 blo = A.bb_cj[2 * cj], bhi = A.bb_cj[2 * cj + 1];
-    if (blo.w == 0.0f) return 0u;
-    if (!(bb_dist2(slo, shi, v, blo, bhi) < A.rl2)) return 0u;
-    unsigned imask = 0u, need = 0u;
-    for (int kk = 0; kk < 8; kk++) {
-        const int ci = 8 * sci + kk;
-        const float4 ilo = A.bb_ci[2 * ci], ihi = A.bb_ci[2 * ci + 1];
-        uint2 m = make_uint2(0u, 0u);
-        if (ilo.w != 0.0f && bb_dist2(ilo, ihi, v, blo, bhi) < A.rl2) {
-            const bool exov = has_partner(X, kk, cj);
-            const bool masked = ilo.w < 4.0f || blo.w < 8.0f || A.mode == NBX_LIST_NONLOCAL ||
-                                (central && (cj >> 2) == sci) || exov;
-            m = make_uint2(0xffffffffu, 0u);
-            if (masked) m = tile_masks(A, ci, cj, exov, central);
-            if ((m.x | m.y) != 0u) {
-                imask |= 1u << kk;
-                if (m.x != 0xffffffffu || m.y != 0u) need = 1u;
-            } else {
-                m = make_uint2(0u, 0u);
-            }
-        }
-        if (pool) {
-            pool->m[kk][0] = m.x;
-            pool->m[kk][1] = m.y;
-        }
-    }
-    return imask | (need << 8);
+    if (blo.w == 0.0f) return false;
+    return bb_dist2(slo, shi, v, blo, bhi) < A.rl2;
 }
 
-template <bool FILL>
+// one (i-cluster k, j-cluster cj) tile of a surviving candidate: (0,0) if it is not in the
+// list, (~0, 0) for a plain tile, explicit masks for filler / diagonal / nonlocal /
+// excluded-partner tiles
+__device__ __forceinline__ uint2 tile_eval(const SearchArgs& A, const WarpEx& X, int sci, int k, int cj,
+                                           float3 v, bool central)
+{
+    const int ci = 8 * sci + k;
+    const float4 ilo = A.bb_ci[2 * ci], ihi = A.bb_ci[2 * ci + 1];
+    const float4 blo = A.bb_cj[2 * cj], bhi = A.bb_cj[2 * cj + 1];
+    if (ilo.w == 0.0f || !(bb_dist2(ilo, ihi, v, blo, bhi) < A.rl2)) return make_uint2(0u, 0u);
+    const bool exov = has_partner(X, k, cj);
+    const bool masked = ilo.w < 4.0f || blo.w < 8.0f || A.mode == NBX_LIST_NONLOCAL ||
+                        (central && (cj >> 2) == sci) || exov;
+    if (!masked) return make_uint2(0xffffffffu, 0u);
+    const uint2 m = tile_masks(A, ci, cj, exov, central);
+    return ((m.x | m.y) != 0u) ? m : make_uint2(0u, 0u);
+}
+
+template <int MODE>
 __global__ void __launch_bounds__(SEARCH_THREADS) k_search(SearchArgs A)
 {
     __shared__ WarpEx s_ex[SEARCH_THREADS / 32];
@@ -172,11 +172,16 @@ __global__ void __launch_bounds__(SEARCH_THREADS) k_search(SearchArgs A)
     const float4 slo = A.bb_sci[2 * sci], shi = A.bb_sci[2 * sci + 1];
     int n_ent = 0, n_cj = 0, n_pool = 0;
     int ent_base = 0, cj_base = 0, pool_base = 0;
-    if (FILL) {
+    if (MODE == SEARCH_FILL) {
         ent_base = A.offsets[sci];
         cj_base = A.offsets[(A.nsci_i + 1) + sci];
         pool_base = 1 + A.offsets[2 * (A.nsci_i + 1) + sci];
+    } else if (MODE == SEARCH_SINGLE) {
+        ent_base = NBX_NSHIFT * sci;
+        cj_base = A.cap_cj * sci;
+        pool_base = A.cap_pool * sci; // private pool slots, 1-based local index stored in meta
     }
+    constexpr bool WRITE = MODE != SEARCH_COUNT;
     if (slo.w != 0.0f) {
         for (int s = 0; s < NBX_NSHIFT; s++) {
             const int sx = s % 3 - 1, sy = (s / 3) % 3 - 1, sz = s / 9 - 1;
@@ -249,27 +254,59 @@ __global__ void __launch_bounds__(SEARCH_THREADS) k_search(SearchArgs A)
                     const int base_o = __shfl_sync(FULL, excl, own);
                     const int ks_o = __shfl_sync(FULL, ks, own);
                     const int cj = 4 * ks_o + (t - base_o);
-                    unsigned res = 0u;
-                    if (t < total) res = eval_candidate(A, X, sci, cj, v, central, slo, shi, nullptr);
-                    const unsigned has = __ballot_sync(FULL, (res & 0xffu) != 0u);
-                    const unsigned pb = __ballot_sync(FULL, (res >> 8) != 0u);
-                    if (FILL && (res & 0xffu)) {
-                        unsigned pidx = 0u;
-                        if (res >> 8) {
-                            pidx = (unsigned)(pool_base + n_pool + __popc(pb & lt));
-                            eval_candidate(A, X, sci, cj, v, central, slo, shi, A.pool_out + pidx);
+                    // phase A: one candidate per lane against the super-cluster box
+                    const bool pass = (t < total) && sci_test(A, sci, cj, v, central, slo, shi);
+                    const unsigned S = __ballot_sync(FULL, pass);
+                    if (pass) X.surv[__popc(S & lt)] = cj;
+                    __syncwarp();
+                    const int ns = __popc(S);
+                    // phase B: lane = (survivor q0 + lane/8, i-cluster lane%8), 4 survivors per pass
+                    const int sub = lane >> 3, k = lane & 7;
+                    const unsigned sublt = (1u << sub) - 1u;
+                    for (int q0 = 0; q0 < ns; q0 += 4) {
+                        const int q = q0 + sub;
+                        const int cjq = (q < ns) ? X.surv[q] : 0;
+                        const uint2 m = (q < ns) ? tile_eval(A, X, sci, k, cjq, v, central) : make_uint2(0u, 0u);
+                        const bool act = (m.x | m.y) != 0u;
+                        const bool need = act && (m.x != 0xffffffffu || m.y != 0u);
+                        const unsigned ab = __ballot_sync(FULL, act);
+                        const unsigned nb = __ballot_sync(FULL, need);
+                        unsigned am = 0u, pm = 0u; // per-survivor: entry emitted / needs a pool entry
+#pragma unroll
+                        for (int u = 0; u < 4; u++) {
+                            am |= ((ab >> (8 * u)) & 0xffu) ? (1u << u) : 0u;
+                            pm |= ((nb >> (8 * u)) & 0xffu) ? (1u << u) : 0u;
                         }
-                        nbx_cj_entry e;
-                        e.cj = cj;
-                        e.meta = (res & 0xffu) | (pidx << 8);
-                        A.cj_out[cj_base + n_cj + __popc(has & lt)] = e;
+                        if (WRITE && ((am >> sub) & 1u)) {
+                            const int cpos = n_cj + __popc(am & sublt);
+                            const int ppos = n_pool + __popc(pm & sublt);
+                            const bool fits = MODE != SEARCH_SINGLE || (cpos < A.cap_cj && ppos < A.cap_pool);
+                            if (fits) {
+                                unsigned pidx = 0u;
+                                if ((pm >> sub) & 1u) {
+                                    pidx = (MODE == SEARCH_SINGLE) ? (unsigned)(ppos + 1) : (unsigned)(pool_base + ppos);
+                                    nbx_mask_pool_entry* pe = A.pool_out + (MODE == SEARCH_SINGLE ? pool_base + ppos : pool_base + ppos);
+                                    pe->m[k][0] = m.x;
+                                    pe->m[k][1] = m.y;
+                                }
+                                if (k == 0) {
+                                    nbx_cj_entry e;
+                                    e.cj = cjq;
+                                    e.meta = ((ab >> (8 * sub)) & 0xffu) | (pidx << 8);
+                                    A.cj_out[cj_base + cpos] = e;
+                                }
+                            } else if (k == 0) {
+                                A.flags[0] = 1;
+                            }
+                        }
+                        n_cj += __popc(am);
+                        n_pool += __popc(pm);
                     }
-                    n_cj += __popc(has);
-                    n_pool += __popc(pb);
+                    __syncwarp();
                 }
             }
             if (n_cj > start_cj) {
-                if (FILL && lane == 0) {
+                if (WRITE && lane == 0) {
                     nbx_sci_entry e;
                     e.sci = sci;
                     e.shift = s;
@@ -281,11 +318,44 @@ __global__ void __launch_bounds__(SEARCH_THREADS) k_search(SearchArgs A)
             }
         }
     }
-    if (!FILL && lane == 0) {
+    if (MODE != SEARCH_FILL && lane == 0) {
         A.counts[sci] = n_ent;
         A.counts[(A.nsci_i + 1) + sci] = n_cj;
         A.counts[2 * (A.nsci_i + 1) + sci] = n_pool;
+        atomicMax(&A.flags[1], n_cj);
+        atomicMax(&A.flags[2], n_pool);
     }
+}
+
+// single pass: move each super-cluster's private output to its scanned position and turn the
+// local pool indices into global ones
+__global__ void k_compact(int nsci, const int* __restrict__ counts, const int* __restrict__ offsets, int cap_cj,
+                          int cap_pool, const nbx_sci_entry* __restrict__ tsci, const nbx_cj_entry* __restrict__ tcj,
+                          const nbx_mask_pool_entry* __restrict__ tpool, nbx_sci_entry* __restrict__ sci_out,
+                          nbx_cj_entry* __restrict__ cj_out, nbx_mask_pool_entry* __restrict__ pool_out)
+{
+    const int lane = threadIdx.x & 31;
+    const int sci = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (sci >= nsci) return;
+    const int n1 = nsci + 1;
+    const int ne = counts[sci], nc = counts[n1 + sci], np = counts[2 * n1 + sci];
+    const int eb = offsets[sci], cb = offsets[n1 + sci], pb = 1 + offsets[2 * n1 + sci];
+    const int src_c = cap_cj * sci;
+    if (lane < ne) {
+        nbx_sci_entry e = tsci[NBX_NSHIFT * sci + lane];
+        e.cj_start += cb - src_c;
+        e.cj_end += cb - src_c;
+        sci_out[eb + lane] = e;
+    }
+    for (int q = lane; q < nc; q += 32) {
+        nbx_cj_entry e = tcj[src_c + q];
+        const unsigned pl = e.meta >> 8;
+        if (pl) e.meta = (e.meta & 0xffu) | ((unsigned)(pb + pl - 1) << 8);
+        cj_out[cb + q] = e;
+    }
+    const uint4* ps = reinterpret_cast<const uint4*>(tpool + (size_t)cap_pool * sci);
+    uint4* pd = reinterpret_cast<uint4*>(pool_out + pb);
+    for (int w = lane; w < 4 * np; w += 32) pd[w] = ps[w];
 }
 
 __global__ void k_pool0(nbx_mask_pool_entry* pool)
@@ -463,6 +533,36 @@ void count_pairs(nbx_ctx* ctx, int l, long long* pairs, long long* slots, cudaSt
     *slots = 32ll * (long long)h[1];
 }
 
+// Row f2 (the paper's post-prune list sort): order the
+// inner list's sci entries longest first, so the persistent force kernel's dynamic
+// scheduler starts the long entries early and the tail is short.  Stable radix sort on the
+// inverted length: deterministic.
+__global__ void k_entry_len(const nbx_sci_entry* __restrict__ sci, int n, unsigned* __restrict__ key,
+                            int* __restrict__ idx)
+{
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n) return;
+    key[e] = 0xffffffffu - (unsigned)(sci[e].cj_end - sci[e].cj_start);
+    idx[e] = e;
+}
+
+static void sort_entries(nbx_ctx* ctx, List& L, cudaStream_t st)
+{
+    const int n = (int)L.n_sci;
+    if (n == 0) return;
+    L.len_key.ensure(n); L.len_key_out.ensure(n); L.order_in.ensure(n); L.order.ensure(n);
+    k_entry_len<<<(n + 255) / 256, 256, 0, st>>>(L.sci_in.p, n, L.len_key.p, L.order_in.p);
+    ctx->launches++;
+    NBX_CUDA(cudaGetLastError());
+    size_t tb = 0;
+    NBX_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, L.len_key.p, L.len_key_out.p, L.order_in.p,
+                                             L.order.p, n, 0, 32, st));
+    L.sort_tmp.ensure(tb + 16);
+    NBX_CUDA(cub::DeviceRadixSort::SortPairs(L.sort_tmp.p, tb, L.len_key.p, L.len_key_out.p, L.order_in.p,
+                                             L.order.p, n, 0, 32, st));
+    ctx->launches += 4;
+}
+
 void prune(nbx_ctx* ctx, int l, int part, int nparts, cudaStream_t st)
 {
     List& L = ctx->list[l];
@@ -476,6 +576,7 @@ void prune(nbx_ctx* ctx, int l, int part, int nparts, cudaStream_t st)
     k_prune<<<(nw * 32 + PRUNE_THREADS - 1) / PRUNE_THREADS, PRUNE_THREADS, 0, st>>>(A);
     ctx->launches++;
     NBX_CUDA(cudaGetLastError());
+    if (ctx->entry_order) sort_entries(ctx, L, st);
 }
 
 void search(nbx_ctx* ctx, int l, cudaStream_t st)
@@ -521,12 +622,30 @@ void search(nbx_ctx* ctx, int l, cudaStream_t st)
     const int n3 = 3 * (nsci + 1);
     L.counts.ensure(n3);
     L.offsets.ensure(n3);
+    L.flags.ensure(4);
     NBX_CUDA(cudaMemsetAsync(L.counts.p, 0, sizeof(int) * n3, st));
+    NBX_CUDA(cudaMemsetAsync(L.flags.p, 0, sizeof(int) * 4, st));
     A.counts = L.counts.p;
     A.offsets = L.offsets.p;
+    A.flags = L.flags.p;
     const int blocks = (nsci * 32 + SEARCH_THREADS - 1) / SEARCH_THREADS;
-    if (nsci > 0) {
-        k_search<false><<<blocks, SEARCH_THREADS, 0, st>>>(A);
+    // Single pass when a previous search sized the per-sci capacities (the list structure
+    // changes little between searches); otherwise, or on overflow, count + fill.
+    const bool single = L.cap_cj > 0 && nsci > 0;
+    if (single) {
+        L.tsci.ensure((size_t)NBX_NSHIFT * nsci);
+        L.tcj.ensure((size_t)L.cap_cj * nsci);
+        L.tpool.ensure((size_t)L.cap_pool * nsci);
+        A.cap_cj = L.cap_cj;
+        A.cap_pool = L.cap_pool;
+        A.sci_out = L.tsci.p;
+        A.cj_out = L.tcj.p;
+        A.pool_out = L.tpool.p;
+        k_search<SEARCH_SINGLE><<<blocks, SEARCH_THREADS, 0, st>>>(A);
+        ctx->launches++;
+        NBX_CUDA(cudaGetLastError());
+    } else if (nsci > 0) {
+        k_search<SEARCH_COUNT><<<blocks, SEARCH_THREADS, 0, st>>>(A);
         ctx->launches++;
         NBX_CUDA(cudaGetLastError());
     }
@@ -538,10 +657,11 @@ void search(nbx_ctx* ctx, int l, cudaStream_t st)
                                                L.offsets.p + k * (nsci + 1), nsci + 1, st));
         ctx->launches++;
     }
-    int tot[3];
+    int tot[3], fl[4];
     for (int k = 0; k < 3; k++)
         NBX_CUDA(cudaMemcpyAsync(&tot[k], L.offsets.p + k * (nsci + 1) + nsci, sizeof(int),
                                  cudaMemcpyDeviceToHost, st));
+    NBX_CUDA(cudaMemcpyAsync(fl, L.flags.p, sizeof(fl), cudaMemcpyDeviceToHost, st));
     NBX_CUDA(cudaStreamSynchronize(st));
     L.n_sci = tot[0];
     L.n_cj = tot[1];
@@ -552,16 +672,24 @@ void search(nbx_ctx* ctx, int l, cudaStream_t st)
     L.cj.ensure(L.n_cj + 1);
     L.cj_in.ensure(L.n_cj + 1);
     L.pool.ensure(L.n_pool);
-    A.sci_out = L.sci.p;
-    A.cj_out = L.cj.p;
-    A.pool_out = L.pool.p;
     k_pool0<<<1, 32, 0, st>>>(L.pool.p);
     ctx->launches++;
-    if (nsci > 0) {
-        k_search<true><<<blocks, SEARCH_THREADS, 0, st>>>(A);
+    if (single && !fl[0]) {
+        k_compact<<<blocks, SEARCH_THREADS, 0, st>>>(nsci, L.counts.p, L.offsets.p, L.cap_cj, L.cap_pool, L.tsci.p,
+                                                     L.tcj.p, L.tpool.p, L.sci.p, L.cj.p, L.pool.p);
+        ctx->launches++;
+        NBX_CUDA(cudaGetLastError());
+    } else if (nsci > 0) {
+        A.sci_out = L.sci.p;
+        A.cj_out = L.cj.p;
+        A.pool_out = L.pool.p;
+        k_search<SEARCH_FILL><<<blocks, SEARCH_THREADS, 0, st>>>(A);
         ctx->launches++;
         NBX_CUDA(cudaGetLastError());
     }
+    // capacities for the next single pass: 25% headroom over this search's maxima
+    L.cap_cj = fl[1] + fl[1] / 4 + 32;
+    L.cap_pool = fl[2] + fl[2] / 4 + 8;
     L.built = true;
     prune(ctx, l, 0, 1, st);
 }

@@ -290,3 +290,25 @@ def test_full_size_water12m_properties(gpu):
     assert_forces(f.cpu().numpy(), fo)
     assert_energies(e, eo)
     assert_virial(vir, viro)
+
+
+def test_repeated_search_single_pass_and_overflow(gpu):
+    """Second and later searches on a context use the single-pass search sized by the previous
+    one; a denser configuration overflows those capacities and falls back to count + fill.
+    Both must stay bit-exact with the oracle."""
+    import torch
+    s = get_system("rnase24k")
+    nb = gpu_nb(s)
+    rng = np.random.default_rng(9)
+    xs = [s.x, (s.x + rng.uniform(-0.05, 0.05, s.x.shape)).astype(np.float32)]
+    dense = s.x.copy()
+    half = s.natoms // 2
+    dense[:half] = (s.x[:half] * 0.55).astype(np.float32)  # squeeze half the atoms: denser lists
+    xs.append(dense)
+    for x in xs:
+        nb.search(to_dev(x))
+        torch.cuda.synchronize()
+        on = O.OracleNonbonded(s)
+        on.search(x)
+        for which in (0, 1):
+            assert_lists_equal(nb.pairlist(which), on.list.export(which), f"repeat list{which}")
