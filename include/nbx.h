@@ -44,6 +44,9 @@ typedef enum {
 
 /* ---- parameters (mirrors the reference's per-system knobs, presets.py:28-49) ------------ */
 enum { NBX_COULOMB_RF = 0, NBX_COULOMB_EWALD = 1 };
+/* LJ modifiers: potential shift (default) or force switch between rvdw_switch and rc
+ * (the CHARMM/STMV flavour of the paper) */
+enum { NBX_LJ_POT_SHIFT = 0, NBX_LJ_FORCE_SWITCH = 1 };
 
 typedef struct nbx_params {
     int32_t coulomb_type; /* NBX_COULOMB_RF or NBX_COULOMB_EWALD                           */
@@ -53,6 +56,8 @@ typedef struct nbx_params {
     float epsilon_r;      /* relative dielectric constant                                  */
     float epsilon_rf;     /* reaction-field dielectric; 0 means infinity                   */
     float ewald_rtol;     /* erfc(beta*rc) = ewald_rtol                                    */
+    int32_t lj_modifier;  /* NBX_LJ_POT_SHIFT or NBX_LJ_FORCE_SWITCH                         */
+    float rvdw_switch;    /* force-switch start r1, 0 <= r1 < rc (ignored for POT_SHIFT)   */
 } nbx_params;
 
 /* Derived constants, computed identically (double, then rounded once) by the library and
@@ -68,6 +73,12 @@ typedef struct nbx_consts {
     float rc2;      /* rc^2                                                               */
     float rlo2;     /* rlist_outer^2                                                      */
     float rli2;     /* rlist_inner^2                                                      */
+    /* force switch: F_a(r) = a r^-(a+1) + A_a (r-r1)^2 + B_a (r-r1)^3 for r1 <= r < rc,
+     * V_a(r) = r^-a - A_a/3 (r-r1)^3 - B_a/4 (r-r1)^4 - C_a  (a = 6, 12; GROMACS convention) */
+    float fsw_r1;
+    float fsw_a6, fsw_b6, fsw_a12, fsw_b12;   /* A_a / a, B_a / a  (tables hold a * c_a)     */
+    float fsw_p6, fsw_q6, fsw_p12, fsw_q12;   /* A_a / 3, B_a / 4                            */
+    float fsw_c6, fsw_c12;                    /* C_a                                          */
 } nbx_consts;
 
 /* ---- pair-list format ----------------------------------------

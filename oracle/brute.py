@@ -18,8 +18,20 @@ def excluded_pairs(excl_offsets, excl_gids):
     return set(zip(a[m].tolist(), b[m].tolist()))
 
 
+def _fsw_terms(r, rc, r1, a):
+    """GROMACS force switch for r^-a on [r1, rc): (F_a(r), V_a(r)) incl. the a r^-(a+1) part."""
+    d = rc - r1
+    A = -a * ((a + 4) * rc - (a + 1) * r1) / (rc ** (a + 2) * d * d)
+    B = a * ((a + 3) * rc - (a + 1) * r1) / (rc ** (a + 2) * d ** 3)
+    C = rc ** -a - A / 3 * d ** 3 - B / 4 * d ** 4
+    t = np.maximum(r - r1, 0.0)
+    F = a * r ** (-(a + 1)) + A * t * t + B * t ** 3
+    V = r ** -a - A / 3 * t ** 3 - B / 4 * t ** 4 - C
+    return F, V
+
+
 def brute_force(x, q, typ, c6c12, excl_offsets, excl_gids, box, consts, coulomb, rc,
-                chunk=2048):
+                chunk=2048, lj_modifier="pot-shift", rvdw_switch=0.0):
     """Returns (f[N,3] float64, (E_lj, E_coul incl. self), virial[3,3])."""
     x = np.asarray(x, np.float64)
     q = np.asarray(q, np.float64)
@@ -56,8 +68,14 @@ def brute_force(x, q, typ, c6c12, excl_offsets, excl_gids, box, consts, coulomb,
         qq = epsfac * q[ai] * q[bj]
         inv = 1.0 / r
         rinv6 = inv**6
-        flj = np.where(ex, 0.0, (12 * c12 * rinv6 * rinv6 - 6 * c6 * rinv6) * inv * inv)  # F/r
-        vlj = np.where(ex, 0.0, c12 * (rinv6 * rinv6 - sh12) - c6 * (rinv6 - sh6))
+        if lj_modifier == "force-switch":
+            F12, V12 = _fsw_terms(r, rc, rvdw_switch, 12.0)
+            F6, V6 = _fsw_terms(r, rc, rvdw_switch, 6.0)
+            flj = np.where(ex, 0.0, (c12 * F12 - c6 * F6) * inv)  # F/r
+            vlj = np.where(ex, 0.0, c12 * V12 - c6 * V6)
+        else:
+            flj = np.where(ex, 0.0, (12 * c12 * rinv6 * rinv6 - 6 * c6 * rinv6) * inv * inv)  # F/r
+            vlj = np.where(ex, 0.0, c12 * (rinv6 * rinv6 - sh12) - c6 * (rinv6 - sh6))
         if coulomb == "rf":
             fc = qq * (np.where(ex, 0.0, inv**3) - 2 * krf)
             vc = qq * (np.where(ex, 0.0, inv) + krf * rr2 - crf)

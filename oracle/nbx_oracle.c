@@ -59,7 +59,30 @@ int ora_derive_consts(const nbx_params* p, nbx_consts* c)
     c->rc2 = (float)(rc * rc);
     c->rlo2 = (float)((double)p->rlist_outer * (double)p->rlist_outer);
     c->rli2 = (float)((double)p->rlist_inner * (double)p->rlist_inner);
+    if (p->lj_modifier == NBX_LJ_FORCE_SWITCH) {
+        const double r1 = p->rvdw_switch, d = rc - r1;
+        double A[2], B[2], C[2];
+        const double al[2] = {6.0, 12.0};
+        for (int k = 0; k < 2; k++) {
+            const double a = al[k], rca2 = pow(rc, a + 2.0);
+            A[k] = -a * ((a + 4.0) * rc - (a + 1.0) * r1) / (rca2 * d * d);
+            B[k] = a * ((a + 3.0) * rc - (a + 1.0) * r1) / (rca2 * d * d * d);
+            C[k] = pow(rc, -a) - A[k] / 3.0 * d * d * d - B[k] / 4.0 * d * d * d * d;
+        }
+        c->fsw_r1 = (float)r1;
+        c->fsw_a6 = (float)(A[0] / 6.0);
+        c->fsw_b6 = (float)(B[0] / 6.0);
+        c->fsw_a12 = (float)(A[1] / 12.0);
+        c->fsw_b12 = (float)(B[1] / 12.0);
+        c->fsw_p6 = (float)(A[0] / 3.0);
+        c->fsw_q6 = (float)(B[0] / 4.0);
+        c->fsw_p12 = (float)(A[1] / 3.0);
+        c->fsw_q12 = (float)(B[1] / 4.0);
+        c->fsw_c6 = (float)C[0];
+        c->fsw_c12 = (float)C[1];
+    }
     if (!(p->rc > 0.0f) || p->rlist_inner < p->rc || p->rlist_outer < p->rlist_inner) return 1;
+    if (p->lj_modifier == NBX_LJ_FORCE_SWITCH && !(p->rvdw_switch >= 0.0f && p->rvdw_switch < p->rc)) return 1;
     return 0;
 }
 
@@ -668,7 +691,7 @@ typedef struct {
  * exclusion-correction (corrb) bits, unmasked tiles have intb = 1, corrb = 0. */
 static inline pairres pair_eval(float dx, float dy, float dz, int masked, int intb, int corrb,
                                 float qi, float qj, float c6, float c12, const nbx_consts* c,
-                                int coul, int energy)
+                                int coul, int energy, int ljmod)
 {
     pairres r = {0.0f, 0.0f, 0.0f, 0};
     float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
@@ -692,10 +715,27 @@ static inline pairres pair_eval(float dx, float dy, float dz, int masked, int in
         float G = ora_ewald_G(z);
         fc = qq * fmaf(-(beta2 * c->beta), G, fint * rinv3);
     }
+    float rsw = 0.0f, rsw2 = 0.0f;
+    if (ljmod == NBX_LJ_FORCE_SWITCH) {
+        /* force switch on [r1, rc): F_a += A_a (r-r1)^2 + B_a (r-r1)^3 */
+        float rr = r2 * rinv;
+        rsw = fmaxf(rr - c->fsw_r1, 0.0f);
+        rsw2 = rsw * rsw;
+        float u = fmaf(c12, fmaf(c->fsw_b12, rsw, c->fsw_a12), -(c6 * fmaf(c->fsw_b6, rsw, c->fsw_a6)));
+        fc = fc + ((u * rsw2) * rinv) * fint;
+    }
     r.fscal = fmaf(flj, rinv2, fc);
     if (energy) {
         const float one6 = 1.0f / 6.0f, one12 = 1.0f / 12.0f;
-        float vlj = fmaf(c12 * one12, fmaf(rinv6, rinv6, -c->sh_lj12), -(c6 * one6) * (rinv6 - c->sh_lj6));
+        float vlj;
+        if (ljmod == NBX_LJ_FORCE_SWITCH) {
+            float rsw3 = rsw2 * rsw;
+            float v12 = fmaf(rinv6, rinv6, -(fmaf(c->fsw_q12, rsw, c->fsw_p12) * rsw3)) - c->fsw_c12;
+            float v6 = (rinv6 - fmaf(c->fsw_q6, rsw, c->fsw_p6) * rsw3) - c->fsw_c6;
+            vlj = fmaf(c12 * one12, v12, -(c6 * one6) * v6);
+        } else {
+            vlj = fmaf(c12 * one12, fmaf(rinv6, rinv6, -c->sh_lj12), -(c6 * one6) * (rinv6 - c->sh_lj6));
+        }
         r.vlj = vlj * fint;
         if (coul == NBX_COULOMB_RF)
             r.vc = qq * fmaf(c->k_rf, r2, fmaf(fint, rinv, -c->c_rf));
@@ -713,7 +753,7 @@ void ora_force(int n_sci, const nbx_sci_entry* sci, const nbx_cj_entry* cj,
 {
     nbx_consts c;
     ora_derive_consts(p, &c);
-    const int coul = p->coulomb_type, energy = (flags & NBX_FORCE_ENERGY) != 0;
+    const int coul = p->coulomb_type, energy = (flags & NBX_FORCE_ENERGY) != 0, ljmod = p->lj_modifier;
     double elj = 0.0, ec = 0.0;
     double fsh[NBX_NSHIFT * 3];
     memset(fsh, 0, sizeof(fsh));
@@ -754,7 +794,7 @@ void ora_force(int n_sci, const nbx_sci_entry* sci, const nbx_cj_entry* cj,
                             const float* cc = c6c12 + 2 * (ti * ntypes + type_j[b]);
                             float c6 = 6.0f * cc[0], c12 = 12.0f * cc[1];
                             pairres r = pair_eval(dx, dy, dz, masked, (im >> bit) & 1, (cm >> bit) & 1,
-                                                  qi, xb[3], c6, c12, &c, coul, energy);
+                                                  qi, xb[3], c6, c12, &c, coul, energy, ljmod);
                             if (!r.valid) continue;
                             float fx = r.fscal * dx, fy = r.fscal * dy, fz = r.fscal * dz;
                             f_i[3 * a + 0] += fx; f_i[3 * a + 1] += fy; f_i[3 * a + 2] += fz;
@@ -820,7 +860,7 @@ void ora_force(int n_sci, const nbx_sci_entry* sci, const nbx_cj_entry* cj,
                                 const float* cc = c6c12 + 2 * (ti * ntypes + type_j[b]);
                                 float c6 = 6.0f * cc[0], c12 = 12.0f * cc[1];
                                 pairres r = pair_eval(dx, dy, dz, masked, (im >> bit) & 1, (cm >> bit) & 1,
-                                                      qi, xb[3], c6, c12, &c, coul, energy);
+                                                      qi, xb[3], c6, c12, &c, coul, energy, ljmod);
                                 if (!r.valid) continue;
                                 float fx = r.fscal * dx, fy = r.fscal * dy, fz = r.fscal * dz;
                                 fiacc[a - 32 * se.sci][0] += fx;

@@ -33,12 +33,14 @@ def build(force: bool = False) -> str:
 class Params(C.Structure):
     _fields_ = [("coulomb_type", C.c_int32), ("rc", C.c_float), ("rlist_outer", C.c_float),
                 ("rlist_inner", C.c_float), ("epsilon_r", C.c_float), ("epsilon_rf", C.c_float),
-                ("ewald_rtol", C.c_float)]
+                ("ewald_rtol", C.c_float), ("lj_modifier", C.c_int32), ("rvdw_switch", C.c_float)]
 
 
 class Consts(C.Structure):
     _fields_ = [(n, C.c_float) for n in ("epsfac", "k_rf", "c_rf", "beta", "sh_ewald", "sh_lj6",
-                                         "sh_lj12", "rc2", "rlo2", "rli2")]
+                                         "sh_lj12", "rc2", "rlo2", "rli2", "fsw_r1", "fsw_a6", "fsw_b6",
+                                         "fsw_a12", "fsw_b12", "fsw_p6", "fsw_q6", "fsw_p12", "fsw_q12",
+                                         "fsw_c6", "fsw_c12")]
 
 
 class ListSizes(C.Structure):
@@ -97,9 +99,9 @@ def _p(a):
 
 
 def make_params(coulomb="ewald", rc=1.0, rlist_outer=1.1, rlist_inner=1.02, epsilon_r=1.0,
-                epsilon_rf=0.0, ewald_rtol=1e-5) -> Params:
+                epsilon_rf=0.0, ewald_rtol=1e-5, lj_modifier="pot-shift", rvdw_switch=0.0) -> Params:
     return Params(1 if coulomb == "ewald" else 0, rc, rlist_outer, rlist_inner, epsilon_r,
-                  epsilon_rf, ewald_rtol)
+                  epsilon_rf, ewald_rtol, {"pot-shift": 0, "force-switch": 1}[lj_modifier], rvdw_switch)
 
 
 def derive_consts(params: Params) -> dict:

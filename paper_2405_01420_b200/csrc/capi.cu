@@ -56,6 +56,30 @@ static int derive(const nbx_params* p, nbx_consts* c)
     c->rc2 = (float)(rc * rc);
     c->rlo2 = (float)((double)p->rlist_outer * (double)p->rlist_outer);
     c->rli2 = (float)((double)p->rlist_inner * (double)p->rlist_inner);
+    if (p->lj_modifier == NBX_LJ_FORCE_SWITCH) {
+        const double r1 = p->rvdw_switch, d = rc - r1;
+        double A[2], B[2], C[2];
+        const double al[2] = {6.0, 12.0};
+        for (int k = 0; k < 2; k++) {
+            const double a = al[k], rca2 = std::pow(rc, a + 2.0);
+            A[k] = -a * ((a + 4.0) * rc - (a + 1.0) * r1) / (rca2 * d * d);
+            B[k] = a * ((a + 3.0) * rc - (a + 1.0) * r1) / (rca2 * d * d * d);
+            C[k] = std::pow(rc, -a) - A[k] / 3.0 * d * d * d - B[k] / 4.0 * d * d * d * d;
+        }
+        c->fsw_r1 = (float)r1;
+        c->fsw_a6 = (float)(A[0] / 6.0);
+        c->fsw_b6 = (float)(B[0] / 6.0);
+        c->fsw_a12 = (float)(A[1] / 12.0);
+        c->fsw_b12 = (float)(B[1] / 12.0);
+        c->fsw_p6 = (float)(A[0] / 3.0);
+        c->fsw_q6 = (float)(B[0] / 4.0);
+        c->fsw_p12 = (float)(A[1] / 3.0);
+        c->fsw_q12 = (float)(B[1] / 4.0);
+        c->fsw_c6 = (float)C[0];
+        c->fsw_c12 = (float)C[1];
+    }
+    if (p->lj_modifier != NBX_LJ_POT_SHIFT && p->lj_modifier != NBX_LJ_FORCE_SWITCH) return 1;
+    if (p->lj_modifier == NBX_LJ_FORCE_SWITCH && !(p->rvdw_switch >= 0.0f && p->rvdw_switch < p->rc)) return 1;
     if (!(p->rc > 0.0f) || p->rlist_inner < p->rc || p->rlist_outer < p->rlist_inner) return 1;
     if (p->coulomb_type != NBX_COULOMB_RF && p->coulomb_type != NBX_COULOMB_EWALD) return 1;
     if (p->coulomb_type == NBX_COULOMB_EWALD && !(p->ewald_rtol > 0.0f && p->ewald_rtol < 1.0f)) return 1;

@@ -92,6 +92,7 @@ struct List {
 
 struct ForceConsts {
     float epsfac, k_rf, two_k_rf, c_rf, beta, beta2, beta3, beta3_monic, sh_ewald, sh_lj6, sh_lj12, rc2, rli2;
+    float fsw_r1, fsw_a6, fsw_b6, fsw_a12, fsw_b12, fsw_p6, fsw_q6, fsw_p12, fsw_q12, fsw_c6, fsw_c12;
 };
 
 } // namespace nbx

@@ -3,15 +3,18 @@
 //
 // Search: one warp per super-cluster.  Per shift image, the warp enumerates the candidate
 // grid columns 32 at a time (one binary search over the column's z-sorted slabs per lane,
-// all in flight together), prefix-sums their j-cluster counts and then tests one candidate
-// j-cluster per lane: super-cluster bounding box, then the 8 i-cluster bounding boxes at
+// all in flight together; columns whose x-y box is out of range are dropped by an exact
+// pre-test), prefix-sums their j-cluster counts and tests the candidates in two phases: one
+// candidate per lane against the super-cluster bounding box, then the survivors' 8
+// i-cluster tiles spread over the lanes (lane = survivor * 8 + i-cluster), all at
 // rlist_outer.  Exclusion masks are only computed for tiles that contain an excluded
 // partner (each i-atom's partners are mapped to their j-cluster through the grid's
 // gid -> slot map into a per-warp shared-memory list), contain filler slots, lie on the
 // diagonal, or belong to the nonlocal (global-id rule) list.  The list is written
-// deterministically: a count pass, exclusive scans, then a fill pass that writes every
-// entry at its ballot/popc rank -- the canonical (sci, shift, cj) order of the CPU oracle
-// (ora_search), bit for bit.
+// deterministically at ballot/popc ranks -- the canonical (sci, shift, cj) order of the CPU
+// oracle (ora_search), bit for bit: in one pass into per-sci private regions (capacity
+// learned from the previous search) plus a compaction, or, for the first search and on
+// overflow, a count pass, exclusive scans and a fill pass.
 //
 // Prune: one warp per sci entry, one cj entry per lane; every active tile tests its atom
 // pairs at rlist_inner and stops at the first hit; kept entries are compacted in order.

@@ -38,12 +38,14 @@ class NbxError(RuntimeError):
 class Params(C.Structure):
     _fields_ = [("coulomb_type", C.c_int32), ("rc", C.c_float), ("rlist_outer", C.c_float),
                 ("rlist_inner", C.c_float), ("epsilon_r", C.c_float), ("epsilon_rf", C.c_float),
-                ("ewald_rtol", C.c_float)]
+                ("ewald_rtol", C.c_float), ("lj_modifier", C.c_int32), ("rvdw_switch", C.c_float)]
 
 
 class Consts(C.Structure):
     _fields_ = [(n, C.c_float) for n in ("epsfac", "k_rf", "c_rf", "beta", "sh_ewald", "sh_lj6",
-                                         "sh_lj12", "rc2", "rlo2", "rli2")]
+                                         "sh_lj12", "rc2", "rlo2", "rli2", "fsw_r1", "fsw_a6", "fsw_b6",
+                                         "fsw_a12", "fsw_b12", "fsw_p6", "fsw_q6", "fsw_p12", "fsw_q12",
+                                         "fsw_c6", "fsw_c12")]
 
 
 class ListSizes(C.Structure):
@@ -112,10 +114,14 @@ def check(code):
         raise NbxError(code, lib().nbx_last_error().decode())
 
 
+LJ_MODIFIERS = {"pot-shift": 0, "force-switch": 1}
+
+
 def make_params(coulomb="ewald", rc=1.0, rlist_outer=1.1, rlist_inner=1.02, epsilon_r=1.0,
-                epsilon_rf=0.0, ewald_rtol=1e-5) -> Params:
+                epsilon_rf=0.0, ewald_rtol=1e-5, lj_modifier="pot-shift", rvdw_switch=0.0) -> Params:
     ct = {"rf": NBX_COULOMB_RF, "ewald": NBX_COULOMB_EWALD}[coulomb]
-    return Params(ct, rc, rlist_outer, rlist_inner, epsilon_r, epsilon_rf, ewald_rtol)
+    return Params(ct, rc, rlist_outer, rlist_inner, epsilon_r, epsilon_rf, ewald_rtol,
+                  LJ_MODIFIERS[lj_modifier], rvdw_switch)
 
 
 def derive_consts(params: Params) -> dict:
@@ -192,6 +198,9 @@ class Nonbonded:
         self.pbc = np.ones(3, np.int32)
         check(lib().nbx_set_box(self.ctx.h, _ptr(self.box), _ptr(self.pbc)))
         self._lo = np.zeros(3, np.float32)
+        self._epoch = 0  # bumped by every search: captured step graphs become stale
+        self._graph = None
+        self._graph_key = None
 
     # -- the four simulated kernels, for real ----------------------------------------------
     def search(self, x, stream=None):
@@ -202,6 +211,8 @@ class Nonbonded:
         check(lib().nbx_grid_build(self.ctx.h, 0, self.n, _dev_ptr(x), None, _ptr(self._lo),
                                    _ptr(self.box), st))
         check(lib().nbx_search(self.ctx.h, LIST_LOCAL, st))
+        self._epoch += 1
+        self._graph = None
 
     def put_x(self, x, stream=None):
         check(lib().nbx_put_x(self.ctx.h, 0, _dev_ptr(x), _stream(self.torch, stream)))
@@ -242,10 +253,42 @@ class Nonbonded:
         self.get_f(out, stream=stream)
         return (out, res) if res is not None else out
 
-    def step(self, x, f, step, energy=False, virial=False, stream=None):
-        """One NB-path MD step with the reference cadence (pipeline.py:222-235)."""
+    def graph_step(self, x, f, prune=False):
+        """X op (+ prune) + force + F op of a non-search step as one CUDA-graph replay.
+
+        The graph is captured on first use for the given (x, f) buffers and recaptured after
+        every search (list buffers may have moved): launch overhead is paid once per search,
+        not per kernel per step (matters for the small boxes, ~4 launches per step)."""
+        torch = self.torch
+        key = (x.data_ptr(), f.data_ptr(), bool(prune), self._epoch)
+        if self._graph is None or self._graph_key != key:
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):  # one eager pass: lazy one-time initialisation
+                self.put_x(x)
+                if prune:
+                    self.prune()
+                self.compute()
+                self.get_f(f)
+            torch.cuda.current_stream().wait_stream(side)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, capture_error_mode="thread_local"):
+                self.put_x(x)
+                if prune:
+                    self.prune()
+                self.compute()
+                self.get_f(f)
+            self._graph, self._graph_key = g, key
+        self._graph.replay()
+
+    def step(self, x, f, step, energy=False, virial=False, stream=None, graphs=False):
+        """One NB-path MD step with the reference cadence (pipeline.py:222-235).
+        graphs=True replays non-search, non-energy steps as a captured CUDA graph."""
         search = step % self.nstlist == 0
         prune = (not search) and self.prune_every and step % self.prune_every == 0
+        if graphs and not search and not (energy or virial) and stream is None:
+            self.graph_step(x, f, prune=bool(prune))
+            return None
         if search:
             self.search(x, stream)  # builds the cluster xyzq buffer from x as well
         else:

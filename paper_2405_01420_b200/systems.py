@@ -45,6 +45,8 @@ class System:
     epsilon_r: float = 1.0
     epsilon_rf: float = 0.0  # 0 = infinity
     ewald_rtol: float = 1e-5
+    lj_modifier: str = "pot-shift"  # or "force-switch" (CHARMM/STMV flavour)
+    rvdw_switch: float = 0.0
     nstlist: int = 100  # presets.py:44
     prune_every: int = 10  # presets.py:45
     dt_fs: float = 2.0  # presets.py:42
@@ -62,7 +64,8 @@ class System:
     def params(self) -> dict:
         return dict(coulomb=self.coulomb, rc=self.rc, rlist_outer=self.rlist_outer,
                     rlist_inner=self.rlist_inner, epsilon_r=self.epsilon_r,
-                    epsilon_rf=self.epsilon_rf, ewald_rtol=self.ewald_rtol)
+                    epsilon_rf=self.epsilon_rf, ewald_rtol=self.ewald_rtol,
+                    lj_modifier=self.lj_modifier, rvdw_switch=self.rvdw_switch)
 
     def expected_pairs(self) -> float:
         """In-cut-off unordered pairs at uniform density."""
@@ -296,6 +299,7 @@ CONFIGS = {
     "rnase24k": dict(desc="RNase-sized 24,024-atom solvated protein-like box, Ewald, rc=1.0 nm"),
     "mem82k": dict(desc="benchMEM-sized 82k-atom membrane-like box, Ewald, prune every 10"),
     "stmv": dict(desc="STMV-sized 1,066,628-atom water/protein box, Ewald, rc=1.2 nm"),
+    "stmv_fsw": dict(desc="STMV box with force-switch LJ (rvdw_switch 1.0 nm, rc 1.2 nm)"),
     "water12m": dict(desc="12M-atom water box, Ewald, rc=1.0 nm"),
 }
 
@@ -312,6 +316,11 @@ def make(name: str, natoms: int | None = None) -> System:
         return membrane_box(natoms or 82000, seed=3, rc=1.0, name="mem82k")
     if name == "stmv":
         return protein_box(natoms or 1066628, seed=4, rc=1.2, frac=0.15, name="stmv")
+    if name == "stmv_fsw":
+        # the paper's STMV flavour: force-switch LJ (rvdw_switch 1.0, rc 1.2)
+        s = protein_box(natoms or 1066628, seed=4, rc=1.2, frac=0.15, name="stmv_fsw")
+        s.lj_modifier, s.rvdw_switch = "force-switch", 1.0
+        return s
     if name == "water12m":
         n = natoms or 12_000_000
         return water_box(n // 3, seed=5, coulomb="ewald", rc=1.0, name="water12m")

@@ -312,3 +312,36 @@ def test_repeated_search_single_pass_and_overflow(gpu):
         on.search(x)
         for which in (0, 1):
             assert_lists_equal(nb.pairlist(which), on.list.export(which), f"repeat list{which}")
+
+
+def test_graph_steps_match_eager(gpu):
+    """CUDA-graph replayed steps (Nonbonded.step(graphs=True)) give the eager forces."""
+    import torch
+    s = get_system("rnase24k")
+    nb_e, nb_g = gpu_nb(s), gpu_nb(s)
+    rng = np.random.default_rng(2)
+    x = to_dev(s.x)
+    fe = torch.empty_like(x)
+    fg = torch.empty_like(x)
+    for step in range(0, 23):
+        nb_e.step(x, fe, step)
+        nb_g.step(x, fg, step, graphs=True)
+        torch.cuda.synchronize()
+        assert torch.equal(fe, fg) or float((fe - fg).abs().max()) < 1e-3 * float(fe.abs().max()), step
+        x.add_(torch.from_numpy(rng.uniform(-0.002, 0.002, s.x.shape).astype(np.float32)).cuda())
+
+
+@pytest.mark.parametrize("natoms", [60000, None])
+def test_force_switch_flavour(gpu, natoms):
+    """Row f3: force-switch LJ kernels (F and VF) vs the oracle; None = full STMV size."""
+    import torch
+    s = get_system("stmv_fsw", natoms)
+    nb, on, xd = run_pair(s)
+    f, (e, vir) = nb.forces(xd, energy=True, virial=True)
+    f2 = nb.forces(xd)
+    torch.cuda.synchronize()
+    fo, eo, viro, _ = on.forces()
+    assert_forces(f.cpu().numpy(), fo)
+    assert_forces(f2.cpu().numpy(), fo)
+    assert_energies(e, eo)
+    assert_virial(vir, viro)

@@ -192,3 +192,20 @@ def test_golden_fixtures():
 def _list_crc(lst):
     import zlib
     return zlib.crc32(lst["sci"].tobytes() + lst["cj"].tobytes() + lst["pool"].tobytes())
+
+
+def test_force_switch_vs_brute_force():
+    """Row f3: force-switch LJ (GROMACS vdw-modifier = force-switch) against float64."""
+    s = systems.make("stmv_fsw", 6000)
+    on = O.OracleNonbonded(s)
+    on.search(s.x)
+    f, e, vir, _ = on.forces()
+    c = O.derive_consts(on.params)
+    fb, eb, vb = brute_force(s.x, s.q, s.type, s.c6c12, s.excl_offsets, s.excl_gids, s.box, c, s.coulomb, s.rc,
+                             lj_modifier="force-switch", rvdw_switch=s.rvdw_switch)
+    assert np.sqrt(((f - fb) ** 2).sum() / (fb**2).sum()) < 5e-6
+    assert abs(e[0] - eb[0]) / abs(eb[0]) < 1e-5
+    assert np.abs(vir - vb).max() / np.abs(vb).max() < 5e-6
+    # the switched force vanishes continuously at rc: a pair just inside rc has ~0 LJ force
+    cf = O.derive_consts(O.make_params(**s.params()))
+    assert cf["fsw_r1"] == np.float32(1.0)
