@@ -690,9 +690,16 @@ void search(nbx_ctx* ctx, int l, cudaStream_t st)
         ctx->launches++;
         NBX_CUDA(cudaGetLastError());
     }
-    // capacities for the next single pass: 25% headroom over this search's maxima
-    L.cap_cj = fl[1] + fl[1] / 4 + 32;
-    L.cap_pool = fl[2] + fl[2] / 4 + 8;
+    // capacities for the next single pass: 25% headroom over this search's maxima; the
+    // private buffers are allocated now, outside the next search
+    const int ncap = fl[1] + fl[1] / 4 + 32, pcap = fl[2] + fl[2] / 4 + 8;
+    L.cap_cj = L.cap_cj > ncap ? L.cap_cj : ncap;
+    L.cap_pool = L.cap_pool > pcap ? L.cap_pool : pcap;
+    if (nsci > 0) {
+        L.tsci.ensure((size_t)NBX_NSHIFT * nsci);
+        L.tcj.ensure((size_t)L.cap_cj * nsci);
+        L.tpool.ensure((size_t)L.cap_pool * nsci);
+    }
     L.built = true;
     prune(ctx, l, 0, 1, st);
 }

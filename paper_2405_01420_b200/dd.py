@@ -185,6 +185,8 @@ class DomainDecomposition:
         self.nstlist = system.nstlist
         self.prune_every = system.prune_every
         self.comm_stream = None
+        self.profile_phases = False  # record per-phase CUDA events in step() (bench breakdown)
+        self.phase_log = []
 
     # ---------------------------------------------------------------------- partitioning
     def _exchange(self, sends, recvs):
@@ -317,10 +319,13 @@ class DomainDecomposition:
         """One NB-path step: returns f_home (a view of the rank's force buffer, overwritten by
         the next step) and, with energy/virial, the all-reduced (energies, virial)."""
         eng = self.engine
+        ev = self._events() if self.profile_phases else None
         if x_home is not None:
             self.x_ext[:self.n_home].copy_(x_home)
         if prune is None:
             prune = bool(self.prune_every) and step % self.prune_every == 0
+        if ev:
+            ev[0].record()
         works = self.halo_x()  # NCCL in flight while the local kernel runs
         eng.put_x(0, self.x_ext[:self.n_home])
         if prune:
@@ -329,12 +334,18 @@ class DomainDecomposition:
         if flags:
             eng.clear_energies()
         eng.force(0, flags)
+        if ev:
+            ev[1].record()
         for w in works:
             w.wait()
+        if ev:
+            ev[2].record()
         eng.put_x(1, self.x_ext[self.n_home:])
         if prune:
             eng.prune(1)
         eng.force(1, flags)
+        if ev:
+            ev[3].record()
         res = None
         if flags:
             e, v = eng.energies()
@@ -345,8 +356,28 @@ class DomainDecomposition:
         eng.get_f(0, self.f_ext[:self.n_home])
         eng.get_f(1, self.f_ext[self.n_home:])
         self.halo_f()
+        if ev:
+            ev[4].record()
+            self.phase_log.append(ev)
         f_home = self.f_ext[:self.n_home]
         return (f_home, res) if res is not None else f_home
+
+    def _events(self):
+        E = self.torch.cuda.Event
+        return [E(enable_timing=True) for _ in range(5)]
+
+    def phase_summary(self):
+        """Mean ms per step of: local (halo issue + local force), halo wait (exposed x halo),
+        nonlocal force, F ops + force halo; from the events of profiled steps."""
+        self.torch.cuda.synchronize()
+        if not self.phase_log:
+            return None
+        names = ["local", "x_halo_exposed", "nonlocal", "f_ops_and_f_halo"]
+        acc = [0.0] * 4
+        for ev in self.phase_log:
+            for k in range(4):
+                acc[k] += ev[k].elapsed_time(ev[k + 1])
+        return {n: a / len(self.phase_log) for n, a in zip(names, acc)}
 
     def count_pairs(self):
         p0, s0 = self.engine.count_pairs(0)
@@ -407,6 +438,12 @@ def bench(args, METRIC, UNIT, FLOPS_PER_PAIR, DESC, ClockSampler, time_cpu_port,
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t[0])
     clk = clocks.stop()
+    # per-phase breakdown on 10 extra (untimed) steps
+    dd.profile_phases = True
+    for k in range(10):
+        dd.step(x_home, step=1)
+    phases = dd.phase_summary()
+    dd.profile_phases = False
     if rank == 0:
         ms_per_step = ms_max / K
         value = pairs_tot * K / (ms_max * 1e-3)
@@ -425,6 +462,7 @@ def bench(args, METRIC, UNIT, FLOPS_PER_PAIR, DESC, ClockSampler, time_cpu_port,
                          "frac": value / 1e12 * fl / world / peak, "traffic": load_traffic(args.config, world),
                          "note": "per GPU, whole NB step (not kernel-only) at N>1"},
             "e2e": None, "gpu_launches": int(launches), "clocks": clk, "searches": n_search,
+            "dd_phases_ms_rank0": phases,
         }
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()

@@ -199,8 +199,7 @@ class Nonbonded:
         check(lib().nbx_set_box(self.ctx.h, _ptr(self.box), _ptr(self.pbc)))
         self._lo = np.zeros(3, np.float32)
         self._epoch = 0  # bumped by every search: captured step graphs become stale
-        self._graph = None
-        self._graph_key = None
+        self._graphs = {}  # (x ptr, f ptr, prune) -> CUDAGraph, for the current epoch
 
     # -- the four simulated kernels, for real ----------------------------------------------
     def search(self, x, stream=None):
@@ -212,7 +211,7 @@ class Nonbonded:
                                    _ptr(self.box), st))
         check(lib().nbx_search(self.ctx.h, LIST_LOCAL, st))
         self._epoch += 1
-        self._graph = None
+        self._graphs = {}
 
     def put_x(self, x, stream=None):
         check(lib().nbx_put_x(self.ctx.h, 0, _dev_ptr(x), _stream(self.torch, stream)))
@@ -260,8 +259,9 @@ class Nonbonded:
         every search (list buffers may have moved): launch overhead is paid once per search,
         not per kernel per step (matters for the small boxes, ~4 launches per step)."""
         torch = self.torch
-        key = (x.data_ptr(), f.data_ptr(), bool(prune), self._epoch)
-        if self._graph is None or self._graph_key != key:
+        key = (x.data_ptr(), f.data_ptr(), bool(prune))
+        g = self._graphs.get(key)
+        if g is None:
             side = torch.cuda.Stream()
             side.wait_stream(torch.cuda.current_stream())
             with torch.cuda.stream(side):  # one eager pass: lazy one-time initialisation
@@ -278,8 +278,8 @@ class Nonbonded:
                     self.prune()
                 self.compute()
                 self.get_f(f)
-            self._graph, self._graph_key = g, key
-        self._graph.replay()
+            self._graphs[key] = g
+        g.replay()
 
     def step(self, x, f, step, energy=False, virial=False, stream=None, graphs=False):
         """One NB-path MD step with the reference cadence (pipeline.py:222-235).
