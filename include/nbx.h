@@ -148,8 +148,9 @@ NBX_API int nbx_grid_build(nbx_ctx* ctx, int grid, int32_t n, const float* x_dev
                            const int32_t* gid_dev, const float lo_host[3],
                            const float size_host[3], void* stream);
 
-/* Build list `list` (LOCAL: grid0 x grid0 half list; NONLOCAL: grid0 i x grid1 j with the
- * global-id rule) at rlist_outer, then prune it to rlist_inner.  Synchronises `stream`
+/* Build list `list` (LOCAL: grid0 x grid0 half list; NONLOCAL: every grid0 i x grid1 j pair,
+ * grid 1 holding a half-shell halo) at rlist_outer, then prune it to
+ * rlist_inner.  Synchronises `stream`
  * once to size the list (count pass -> exact allocation -> fill pass).                   */
 NBX_API int nbx_search(nbx_ctx* ctx, int list, void* stream);
 

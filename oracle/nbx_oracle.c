@@ -535,7 +535,6 @@ ora_list* ora_search(const ora_grid* gi, const ora_grid* gj, int mode, const nbx
                                 if (!(bb_dist2(gi->bb_ci + 6 * ci, v, bj) < rl2)) continue;
                                 int exov = !(gi->exhi_ci[ci] < gj->glo_cj[cj] || gi->exlo_ci[ci] > gj->ghi_cj[cj]);
                                 int masked = gi->nreal_ci[ci] < 4 || gj->nreal_cj[cj] < 8 ||
-                                             mode == NBX_LIST_NONLOCAL ||
                                              (central && (cj >> 2) == sci) || exov;
                                 uint32_t im = 0xffffffffu, cm = 0u;
                                 if (masked) {
@@ -548,7 +547,7 @@ ora_list* ora_search(const ora_grid* gi, const ora_grid* gj, int mode, const nbx
                                             int b = 8 * cj + j;
                                             if (gj->order[b] < 0) continue;
                                             int gb = gj->gid[b];
-                                            int present = (mode == NBX_LIST_LOCAL) ? !(central && b <= a) : (ga < gb);
+                                            int present = (mode == NBX_LIST_LOCAL) ? !(central && b <= a) : 1;
                                             if (!present) continue;
                                             uint32_t bit = 1u << (i * 8 + j);
                                             if (exov && is_excluded(gi, ga, gb)) cm |= bit; else im |= bit;

@@ -10,7 +10,7 @@
 // rlist_outer.  Exclusion masks are only computed for tiles that contain an excluded
 // partner (each i-atom's partners are mapped to their j-cluster through the grid's
 // gid -> slot map into a per-warp shared-memory list), contain filler slots, lie on the
-// diagonal, or belong to the nonlocal (global-id rule) list.  The list is written
+// diagonal (the nonlocal list has no diagonal: every home x halo pair is computed there).  The list is written
 // deterministically at ballot/popc ranks -- the canonical (sci, shift, cj) order of the CPU
 // oracle (ora_search), bit for bit: in one pass into per-sci private regions (capacity
 // learned from the previous search) plus a compaction, or, for the first search and on
@@ -95,7 +95,7 @@ __device__ uint2 tile_masks(const SearchArgs& A, int ci, int cj, bool exov, bool
             const int b = 8 * cj + j;
             if (A.order_j[b] < 0) continue;
             const int gb = A.gid_j[b];
-            const bool present = (A.mode == NBX_LIST_LOCAL) ? !(central && b <= a) : (ga < gb);
+            const bool present = (A.mode == NBX_LIST_LOCAL) ? !(central && b <= a) : true;
             if (!present) continue;
             bool ex = false;
             for (int e = e0; e < e1; e++) ex |= (A.excl_gid[e] == gb);
@@ -136,8 +136,7 @@ __device__ __forceinline__ uint2 tile_eval(const SearchArgs& A, const WarpEx& X,
     const float4 blo = A.bb_cj[2 * cj], bhi = A.bb_cj[2 * cj + 1];
     if (ilo.w == 0.0f || !(bb_dist2(ilo, ihi, v, blo, bhi) < A.rl2)) return make_uint2(0u, 0u);
     const bool exov = has_partner(X, k, cj);
-    const bool masked = ilo.w < 4.0f || blo.w < 8.0f || A.mode == NBX_LIST_NONLOCAL ||
-                        (central && (cj >> 2) == sci) || exov;
+    const bool masked = ilo.w < 4.0f || blo.w < 8.0f || (central && (cj >> 2) == sci) || exov;
     if (!masked) return make_uint2(0xffffffffu, 0u);
     const uint2 m = tile_masks(A, ci, cj, exov, central);
     return ((m.x | m.y) != 0u) ? m : make_uint2(0u, 0u);

@@ -11,10 +11,14 @@ simulated time; here it is real:
     point-to-point sends/receives batched per pulse (no host sync, unlike the paper's
     CPU-initiated MPI, PAPER.md:99);
   * halo width = rlist_outer, staged pulses x -> y -> z forward edge/corner atoms;
-    every rank imports the full shell (both faces of each split dimension);
-  * every cross-domain pair is computed exactly once, on the rank whose home atom has the
-    smaller global id (the nonlocal list's masks encode it, include/nbx.h NBX_LIST_NONLOCAL);
-    forces on imported atoms go back through the reverse pulses and are accumulated by
+  * half-shell import: a rank imports an atom of the domain at offset o (components in
+    {-1, 0, 1} per split dimension, in domain units) iff the first non-zero component of o
+    is +1.  For every cross-domain pair exactly one of o and -o qualifies, so each pair is
+    computed exactly once, on one rank, as a plain home x halo pair of the nonlocal list (no
+    masks, no halo-halo pairs).  In pulse d this means: send to the down neighbour the home
+    and imported atoms near the lower face, and to the up neighbour only the imported atoms
+    near the upper face (home atoms sent up would arrive with offset -1 in dimension d);
+  * forces on imported atoms go back through the reverse pulses and are accumulated by
     the owner (z -> y -> x);
   * atoms are (re)assigned to domains at search steps from the global coordinates.
 
@@ -230,8 +234,12 @@ class DomainDecomposition:
             c[d] = self.coord[d] + 1
             p.up_peer = coords_rank(c, self.dims)
             lo_d, hi_d = lo[d], lo[d] + self.D[d]
+            # half-shell import: down-going messages carry home and imported atoms near the
+            # lower face; up-going ones only imported atoms near the upper face (see header)
             p.down_idx = torch.nonzero(X[:, d] < lo_d + self.rl).flatten().to(torch.int32)
-            p.up_idx = torch.nonzero(X[:, d] >= hi_d - self.rl).flatten().to(torch.int32)
+            up = (X[:, d] >= hi_d - self.rl)
+            up[:self.n_home] = False
+            p.up_idx = torch.nonzero(up).flatten().to(torch.int32)
             sd = np.zeros(3, np.float32)
             su = np.zeros(3, np.float32)
             if self.coord[d] == 0:
