@@ -409,6 +409,8 @@ def bench(args, METRIC, UNIT, FLOPS_PER_PAIR, DESC, ClockSampler, time_cpu_port,
     dd = DomainDecomposition(s, rank, world, lambda sy, pbc: NbxEngine(sy, local, pbc), device=dev)
     xg = torch.from_numpy(s.x).to(dev)
     peak = dd.engine.fma_peak()
+    dd.repartition(xg)  # setup: first search sizes the lists and the single-pass buffers
+    dd.step(None, step=0, prune=False)
     dd.repartition(xg)
     x_home = dd.x_ext[:dd.n_home].clone()
     for k in range(1, args.warmup):
@@ -426,17 +428,22 @@ def bench(args, METRIC, UNIT, FLOPS_PER_PAIR, DESC, ClockSampler, time_cpu_port,
     torch.cuda.synchronize()
     l0 = dd.engine.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(K + 1)]
     e0.record(st)
     n_search = 0
+    search_steps = []
     for k in range(K):
         step = args.warmup + k
+        evs[k].record(st)
         if step % s.nstlist == 0:
             dd.repartition(xg)  # atoms re-assigned from the global coordinates
             n_search += 1
+            search_steps.append(k)
             x_home = dd.x_ext[:dd.n_home].clone()
             dd.step(None, step=step, prune=False)
         else:
             dd.step(x_home, step=step)
+    evs[K].record(st)
     e1.record(st)
     torch.cuda.synchronize()
     dist.barrier()
@@ -446,6 +453,8 @@ def bench(args, METRIC, UNIT, FLOPS_PER_PAIR, DESC, ClockSampler, time_cpu_port,
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t[0])
     clk = clocks.stop()
+    step_ms = sorted(evs[k].elapsed_time(evs[k + 1]) for k in range(K))
+    search_ms = [evs[k].elapsed_time(evs[k + 1]) for k in search_steps]
     # per-phase breakdown on 10 extra (untimed) steps
     dd.profile_phases = True
     for k in range(10):
@@ -471,6 +480,7 @@ def bench(args, METRIC, UNIT, FLOPS_PER_PAIR, DESC, ClockSampler, time_cpu_port,
                          "note": "per GPU, whole NB step (not kernel-only) at N>1"},
             "e2e": None, "gpu_launches": int(launches), "clocks": clk, "searches": n_search,
             "dd_phases_ms_rank0": phases,
+            "step_ms_rank0": {"median": step_ms[K // 2], "max": step_ms[-1], "search_steps": search_ms},
         }
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
