@@ -37,10 +37,12 @@ DESC = {
     "rnase24k": "RNase-sized 24,024-atom solvated protein-like box, Ewald real-space, rc=1.0 nm",
     "mem82k": "benchMEM-sized 82k-atom membrane-like box, LJ + Ewald, dynamic pruning every 10 steps",
     "stmv": "STMV-sized 1,066,628-atom water/protein box, Ewald, rc=1.2 nm",
+    "stmv_fsw": "STMV-sized box with force-switch LJ (rvdw_switch 1.0 nm, rc 1.2 nm), Ewald",
     "water12m": "12M-atom water box, Ewald, rc=1.0 nm (strong-scaling sweep 1/2/4/8)",
 }
 L2_BYTES = 126 * 1024 * 1024
-NATOMS = {"water3k": 3000, "rnase24k": 24024, "mem82k": 82000, "stmv": 1066628, "water12m": 12_000_000}
+NATOMS = {"water3k": 3000, "rnase24k": 24024, "mem82k": 82000, "stmv": 1066628, "stmv_fsw": 1066628,
+          "water12m": 12_000_000}
 
 
 def parse():
@@ -131,7 +133,8 @@ def load_traffic(config, n):
 def cpu_sample_system(config):
     """A bounded sample of the workload for the CPU port: same generator/parameters, fewer atoms."""
     from paper_2405_01420_b200 import systems
-    n = {"water3k": None, "rnase24k": None, "mem82k": 24000, "stmv": 48000, "water12m": 48000}[config]
+    n = {"water3k": None, "rnase24k": None, "mem82k": 24000, "stmv": 48000, "stmv_fsw": 48000,
+         "water12m": 48000}[config]
     return systems.make(config, n), n
 
 
