@@ -12,8 +12,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "scratch", "variants")
 VARIANTS = {
     "base": [],
-    "pair": ["-DNBX_PAIRTILE=1"],
-    "pair_t160b4": ["-DNBX_PAIRTILE=1", "-DNBX_FORCE_THREADS=160", "-DNBX_FORCE_MINB=4"],
+    "xismem_b2": ["-DNBX_XI_SMEM=1"],
+    "xismem_b3": ["-DNBX_XI_SMEM=1", "-DNBX_FORCE_MINB=3"],
+    "xismem_t128b6": ["-DNBX_XI_SMEM=1", "-DNBX_FORCE_THREADS=128", "-DNBX_FORCE_MINB=6"],
 }
 
 
