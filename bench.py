@@ -79,6 +79,16 @@ class ClockSampler:
                                          stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
+            return self
+        # nvidia-smi's NVML start-up contends with this process's CUDA calls for a fraction of a
+        # second: wait for its first sample so the start-up never lands in a timed region
+        t0 = time.time()
+        while time.time() - t0 < 5.0:
+            self.f.flush()
+            if os.path.getsize(self.f.name) > 0:
+                break
+            time.sleep(0.05)
+        time.sleep(0.3)
         return self
 
     def stop(self):
