@@ -194,8 +194,14 @@ def run_single(args):
     peak = nb.fma_peak_tflops()
 
     # warm-up steps 0..W-1 (step 0 is a search step)
+    # small boxes are launch-bound: replay non-search steps as CUDA graphs (the force kernel
+    # time is then taken from a back-to-back loop on the same stream right after)
+    graphs = s.natoms < 500_000
     for k in range(args.warmup):
-        nb.step(x, f, k)
+        nb.step(x, f, k, graphs=graphs)
+    if graphs:  # instantiate both step graphs before the timed region
+        nb.graph_step(x, f, prune=True)
+        nb.graph_step(x, f, prune=False)
     torch.cuda.synchronize()
     pairs, slots = nb.count_pairs()
     sizes = nb.list_sizes()
@@ -211,9 +217,6 @@ def run_single(args):
     torch.cuda.synchronize()
     l0 = nb.launch_count()
     n_search = n_prune = 0
-    # small boxes are launch-bound: replay non-search steps as CUDA graphs (the force kernel
-    # time is then taken from a back-to-back loop on the same stream right after)
-    graphs = s.natoms < 500_000
     for k in range(K):
         step = args.warmup + k
         if flush:
@@ -238,12 +241,8 @@ def run_single(args):
             nb.get_f(f)
         ev[k][1].record(st)
     torch.cuda.synchronize()
-    # graph replays are not counted by the library's launch counter: per replayed step it
-    # launches put_x + force + get_f (+ prune + order sort on prune steps)
-    launches = nb.launch_count() - l0
+    launches = nb.launch_count() - l0  # graph launches are counted per kernel node by the library
     if graphs:
-        launches += sum(3 + (1 if ((args.warmup + k) % s.prune_every == 0) else 0)
-                        for k in range(K) if (args.warmup + k) % s.nstlist != 0)
         for k in range(K):
             evf[k][0].record(st)
             nb.compute()
@@ -306,6 +305,8 @@ def run_single(args):
         "pairs_per_step": pairs,
         "pair_slots_per_step": slots,
         "cluster_efficiency": pairs / slots if slots else None,
+        "step_ms": {"median": sorted(step_ms)[K // 2], "max": max(step_ms),
+                    "search_steps": [step_ms[k] for k in range(K) if (args.warmup + k) % s.nstlist == 0]},
         "kernels_ms": {"force_avg": t_force, "step_avg": ms_per_step,
                        "searches": n_search, "prunes": n_prune},
         "roofline": {"bound": "fp32", "kernel": "k_force (NBNXM force, F only)", "achieved": achieved,

@@ -174,6 +174,14 @@ NBX_API int nbx_force(nbx_ctx* ctx, int list, uint32_t flags, void* stream);
  * the grid-build input, and clear the cluster buffer for the next step.                  */
 NBX_API int nbx_get_f(nbx_ctx* ctx, int grid, float* f_dev, int accumulate, void* stream);
 
+/* ---- one non-search MD step as a CUDA graph (pipeline.py:222-235 minus the search step) *
+ * nbx_put_x(0) [+ nbx_prune(LOCAL, 0, 1) with NBX_STEP_PRUNE] + nbx_force(LOCAL, F only) +
+ * nbx_get_f(0) as one graph launch on `stream`.  Graphs are captured natively per
+ * (x_dev, f_dev, what) and refreshed in place after a search / grid build / box or
+ * topology change, so the small-box step is not launch-bound.                             */
+#define NBX_STEP_PRUNE 1u
+NBX_API int nbx_step_graph(nbx_ctx* ctx, const float* x_dev, float* f_dev, uint32_t what, void* stream);
+
 /* Energies and virial accumulated since the last clear.  Reads grid buffers, so call it
  * after nbx_force and BEFORE nbx_get_f.  e_host[2] = {E_lj, E_coul incl. self term},
  * virial_host[9] = -1/2 sum x (x) f - 1/2 sum s (x) fshift (row-major).  Synchronises.    */

@@ -157,6 +157,7 @@ NBX_API int nbx_create(int device, const nbx_params* p, nbx_ctx** out)
     // 12M box the longest-first order costs L2 locality (force kernel +6%), and the tail it
     // removes is ~3% (ncu sm__cycles_active min/max) -- see DESIGN.md section 5
     if (const char* eo = std::getenv("NBX_ENTRY_ORDER")) ctx->entry_order = std::atoi(eo);
+    if (const char* fs = std::getenv("NBX_FORCE_SPLIT")) ctx->force_split = std::atoi(fs);
     *out = ctx;
     return NBX_OK;
     NBX_GUARD_END
@@ -183,6 +184,8 @@ NBX_API int nbx_destroy(nbx_ctx* ctx)
     }
     ctx->q_g.release(); ctx->type_g.release(); ctx->excl_off_g.release(); ctx->excl_gid_g.release();
     ctx->c6c12s.release(); ctx->acc.release(); ctx->sumq2.release(); ctx->counter.release();
+    for (auto& g : ctx->graphs) cudaGraphExecDestroy(g.exec);
+    if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
     delete ctx;
     return NBX_OK;
     NBX_GUARD_END
@@ -223,6 +226,7 @@ NBX_API int nbx_set_topology(nbx_ctx* ctx, int32_t n, const float* q, const int3
     ctx->c6c12s.ensure(t.size());
     NBX_CUDA(cudaMemcpy(ctx->c6c12s.p, t.data(), sizeof(float2) * t.size(), cudaMemcpyHostToDevice));
     ctx->have_topology = true;
+    ctx->epoch++;
     if (ctx->have_box)
         ctx->density = (double)n / ((double)ctx->box[0] * (double)ctx->box[1] * (double)ctx->box[2]);
     return NBX_OK;
@@ -244,6 +248,7 @@ NBX_API int nbx_set_box(nbx_ctx* ctx, const float box[3], const int32_t pbc[3])
         ctx->pbc[d] = per ? 1 : 0;
     }
     ctx->have_box = true;
+    ctx->epoch++;
     if (ctx->have_topology)
         ctx->density = (double)ctx->natoms_global / ((double)box[0] * (double)box[1] * (double)box[2]);
     return NBX_OK;
@@ -263,6 +268,7 @@ NBX_API int nbx_grid_build(nbx_ctx* ctx, int grid, int32_t n, const float* x, co
     for (int d = 0; d < 3; d++)
         if (!(size[d] > 0.0f)) return fail(NBX_EINVAL, "grid region size must be positive");
     grid_build(ctx, grid, n, x, gid, lo, size, (cudaStream_t)stream);
+    ctx->epoch++;
     // a new grid invalidates the lists built on it
     ctx->list[0].built = ctx->list[0].built && grid != 0;
     ctx->list[1].built = false;
@@ -278,6 +284,7 @@ NBX_API int nbx_search(nbx_ctx* ctx, int list, void* stream)
     if (!ctx->grid[0].built || (list == 1 && !ctx->grid[1].built))
         return fail(NBX_EINVAL, "build the grid(s) first");
     search(ctx, list, (cudaStream_t)stream);
+    ctx->epoch++;
     return NBX_OK;
     NBX_GUARD_END
 }
@@ -321,6 +328,70 @@ NBX_API int nbx_get_f(nbx_ctx* ctx, int grid, float* f, int accumulate, void* st
     if (grid < 0 || grid > 1 || !ctx->grid[grid].built) return fail(NBX_EINVAL, "grid not built");
     if (!f && ctx->grid[grid].n > 0) return fail(NBX_EINVAL, "null force buffer");
     get_f(ctx, grid, f, accumulate, (cudaStream_t)stream);
+    return NBX_OK;
+    NBX_GUARD_END
+}
+
+// X op (+ prune) + force + F op of a non-search MD step of the LOCAL list as one graph
+// launch.  Captured (relaxed mode, on a private stream: nothing executes during capture)
+// on first use for (x, f, what) and refreshed in place after anything bumped ctx->epoch.
+NBX_API int nbx_step_graph(nbx_ctx* ctx, const float* x, float* f, uint32_t what, void* stream)
+{
+    NBX_GUARD_BEGIN
+    NBX_CHECK_CTX(ctx);
+    if (!ctx->list[0].built) return fail(NBX_EINVAL, "list not built");
+    if (!x || !f) return fail(NBX_EINVAL, "null coordinates or force buffer");
+    if (what & ~(uint32_t)NBX_STEP_PRUNE) return fail(NBX_EINVAL, "unknown step flags");
+    nbx_ctx::StepGraph* g = nullptr;
+    for (auto& e : ctx->graphs)
+        if (e.x == x && e.f == f && e.what == what) g = &e;
+    if (!g || g->epoch != ctx->epoch) {
+        if (!ctx->cap_stream)
+            NBX_CUDA(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+        cudaStream_t cs = ctx->cap_stream;
+        const int64_t l0 = ctx->launches;
+        cudaGraph_t graph = nullptr;
+        NBX_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
+        try {
+            put_x(ctx, 0, x, cs);
+            if (what & NBX_STEP_PRUNE) prune(ctx, 0, 0, 1, cs);
+            force(ctx, 0, 0, cs);
+            get_f(ctx, 0, f, 0, cs);
+        } catch (...) {
+            cudaStreamEndCapture(cs, &graph);
+            if (graph) cudaGraphDestroy(graph);
+            ctx->launches = l0;
+            throw;
+        }
+        NBX_CUDA(cudaStreamEndCapture(cs, &graph));
+        const int kernels = (int)(ctx->launches - l0);
+        ctx->launches = l0;
+        bool updated = false;
+        if (g) {
+            cudaGraphExecUpdateResultInfo info;
+            updated = cudaGraphExecUpdate(g->exec, graph, &info) == cudaSuccess;
+            if (!updated) {
+                cudaGetLastError();
+                cudaGraphExecDestroy(g->exec);
+            }
+        } else {
+            ctx->graphs.push_back(nbx_ctx::StepGraph{x, f, what, 0, 0, nullptr});
+            g = &ctx->graphs.back();
+        }
+        if (!updated) {
+            cudaError_t e = cudaGraphInstantiate(&g->exec, graph, 0);
+            if (e != cudaSuccess) {
+                cudaGraphDestroy(graph);
+                ctx->graphs.erase(ctx->graphs.begin() + (g - ctx->graphs.data()));
+                NBX_CUDA(e);
+            }
+        }
+        cudaGraphDestroy(graph);
+        g->epoch = ctx->epoch;
+        g->kernels = kernels;
+    }
+    NBX_CUDA(cudaGraphLaunch(g->exec, (cudaStream_t)stream));
+    ctx->launches += g->kernels;
     return NBX_OK;
     NBX_GUARD_END
 }

@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <vector>
 
 #include "../../include/nbx.h"
 
@@ -117,7 +118,22 @@ struct nbx_ctx {
     nbx::DBuf<double> sumq2;  // [2] per grid
     nbx::DBuf<int> counter;   // work counters [8]
     int64_t launches = 0;
+    int force_split = 0; // > 0: fixed work items per sci entry (env NBX_FORCE_SPLIT), 0: auto
     int entry_order = 0; // 0: list order (spatially coherent), 1: longest first (env NBX_ENTRY_ORDER)
+    // nbx_step_graph: natively captured X op (+ prune) + force + F op, one per (x, f, what);
+    // `epoch` is bumped by every call that can move list/grid buffers or change constants,
+    // and a stale graph is refreshed with cudaGraphExecUpdate (no re-instantiation).
+    struct StepGraph {
+        const float* x;
+        float* f;
+        uint32_t what;
+        uint64_t epoch;
+        int kernels;
+        cudaGraphExec_t exec;
+    };
+    uint64_t epoch = 1;
+    std::vector<StepGraph> graphs;
+    cudaStream_t cap_stream = nullptr;
 };
 
 namespace nbx {

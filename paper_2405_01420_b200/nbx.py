@@ -64,7 +64,7 @@ POOL_DTYPE = np.dtype(("<u4", (8, 2)))
 # every symbol include/nbx.h declares (checked by tests/test_capi.py)
 EXPORTS = ["nbx_last_error", "nbx_version", "nbx_derive_consts", "nbx_create", "nbx_destroy",
            "nbx_set_topology", "nbx_set_box", "nbx_grid_build", "nbx_search", "nbx_put_x",
-           "nbx_prune", "nbx_force", "nbx_get_f", "nbx_energies", "nbx_clear_energies",
+           "nbx_prune", "nbx_force", "nbx_get_f", "nbx_step_graph", "nbx_energies", "nbx_clear_energies",
            "nbx_grid_info_get", "nbx_grid_export", "nbx_list_sizes_get", "nbx_list_export",
            "nbx_count_pairs", "nbx_fma_peak", "nbx_launch_count", "nbx_halo_pack_x", "nbx_halo_unpack_add_f"]
 
@@ -93,6 +93,7 @@ def lib():
         L.nbx_prune.argtypes = [vp, C.c_int, C.c_int, C.c_int, vp]
         L.nbx_force.argtypes = [vp, C.c_int, u32, vp]
         L.nbx_get_f.argtypes = [vp, C.c_int, vp, C.c_int, vp]
+        L.nbx_step_graph.argtypes = [vp, vp, vp, u32, vp]
         L.nbx_energies.argtypes = [vp, vp, vp, vp]
         L.nbx_clear_energies.argtypes = [vp, vp]
         L.nbx_grid_info_get.argtypes = [vp, C.c_int, C.POINTER(GridInfo)]
@@ -198,8 +199,6 @@ class Nonbonded:
         self.pbc = np.ones(3, np.int32)
         check(lib().nbx_set_box(self.ctx.h, _ptr(self.box), _ptr(self.pbc)))
         self._lo = np.zeros(3, np.float32)
-        self._epoch = 0  # bumped by every search: captured step graphs become stale
-        self._graphs = {}  # (x ptr, f ptr, prune) -> CUDAGraph, for the current epoch
 
     # -- the four simulated kernels, for real ----------------------------------------------
     def search(self, x, stream=None):
@@ -210,8 +209,6 @@ class Nonbonded:
         check(lib().nbx_grid_build(self.ctx.h, 0, self.n, _dev_ptr(x), None, _ptr(self._lo),
                                    _ptr(self.box), st))
         check(lib().nbx_search(self.ctx.h, LIST_LOCAL, st))
-        self._epoch += 1
-        self._graphs = {}
 
     def put_x(self, x, stream=None):
         check(lib().nbx_put_x(self.ctx.h, 0, _dev_ptr(x), _stream(self.torch, stream)))
@@ -252,42 +249,23 @@ class Nonbonded:
         self.get_f(out, stream=stream)
         return (out, res) if res is not None else out
 
-    def graph_step(self, x, f, prune=False):
-        """X op (+ prune) + force + F op of a non-search step as one CUDA-graph replay.
+    def graph_step(self, x, f, prune=False, stream=None):
+        """X op (+ prune) + force + F op of a non-search step as one CUDA-graph launch.
 
-        The graph is captured on first use for the given (x, f) buffers and recaptured after
-        every search (list buffers may have moved): launch overhead is paid once per search,
-        not per kernel per step (matters for the small boxes, ~4 launches per step)."""
-        torch = self.torch
-        key = (x.data_ptr(), f.data_ptr(), bool(prune))
-        g = self._graphs.get(key)
-        if g is None:
-            side = torch.cuda.Stream()
-            side.wait_stream(torch.cuda.current_stream())
-            with torch.cuda.stream(side):  # one eager pass: lazy one-time initialisation
-                self.put_x(x)
-                if prune:
-                    self.prune()
-                self.compute()
-                self.get_f(f)
-            torch.cuda.current_stream().wait_stream(side)
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, capture_error_mode="thread_local"):
-                self.put_x(x)
-                if prune:
-                    self.prune()
-                self.compute()
-                self.get_f(f)
-            self._graphs[key] = g
-        g.replay()
+        The graph is captured natively in libnbx.so (nbx_step_graph) per (x, f, prune) and
+        refreshed in place after every search, so launch overhead is paid once per step
+        (matters for the small boxes, ~4 launches per step) and no capture ever runs on the
+        caller's stream."""
+        check(lib().nbx_step_graph(self.ctx.h, _dev_ptr(x), _dev_ptr(f), 1 if prune else 0,
+                                   _stream(self.torch, stream)))
 
     def step(self, x, f, step, energy=False, virial=False, stream=None, graphs=False):
         """One NB-path MD step with the reference cadence (pipeline.py:222-235).
         graphs=True replays non-search, non-energy steps as a captured CUDA graph."""
         search = step % self.nstlist == 0
         prune = (not search) and self.prune_every and step % self.prune_every == 0
-        if graphs and not search and not (energy or virial) and stream is None:
-            self.graph_step(x, f, prune=bool(prune))
+        if graphs and not search and not (energy or virial):
+            self.graph_step(x, f, prune=bool(prune), stream=stream)
             return None
         if search:
             self.search(x, stream)  # builds the cluster xyzq buffer from x as well

@@ -315,20 +315,24 @@ def test_repeated_search_single_pass_and_overflow(gpu):
 
 
 def test_graph_steps_match_eager(gpu):
-    """CUDA-graph replayed steps (Nonbonded.step(graphs=True)) give the eager forces."""
+    """CUDA-graph replayed steps (Nonbonded.step(graphs=True), nbx_step_graph) give the eager
+    forces, across several searches (graphs refreshed in place) and prune steps."""
+    import dataclasses
     import torch
-    s = get_system("rnase24k")
+    s = dataclasses.replace(get_system("rnase24k"), nstlist=20, prune_every=5)
     nb_e, nb_g = gpu_nb(s), gpu_nb(s)
     rng = np.random.default_rng(2)
     x = to_dev(s.x)
     fe = torch.empty_like(x)
     fg = torch.empty_like(x)
-    for step in range(0, 23):
+    l0 = nb_g.launch_count()
+    for step in range(0, 67):
         nb_e.step(x, fe, step)
         nb_g.step(x, fg, step, graphs=True)
         torch.cuda.synchronize()
         assert torch.equal(fe, fg) or float((fe - fg).abs().max()) < 1e-3 * float(fe.abs().max()), step
         x.add_(torch.from_numpy(rng.uniform(-0.002, 0.002, s.x.shape).astype(np.float32)).cuda())
+    assert nb_g.launch_count() - l0 >= 67 * 3  # graph replays count their kernel nodes
 
 
 @pytest.mark.parametrize("natoms", [60000, None])
