@@ -182,6 +182,30 @@ NBX_API int nbx_get_f(nbx_ctx* ctx, int grid, float* f_dev, int accumulate, void
 #define NBX_STEP_PRUNE 1u
 NBX_API int nbx_step_graph(nbx_ctx* ctx, const float* x_dev, float* f_dev, uint32_t what, void* stream);
 
+/* ---- NVLink peer-memory DD halo (row e; replaces the halo pulses of pipeline.py:273-278,
+ * 363-380 and the reverse force pulses of pipeline.py:403-418 for force-only steps) ----- *
+ * One process per GPU on one NVSwitch node.  Each rank allocates an IPC-shared region
+ * (flags | published home x | force inbox) for `capacity` home atoms (same on all ranks),
+ * exchanges the NBX_PEER_HANDLE_BYTES handles (e.g. an all-gather), opens the others', and
+ * after every repartition maps its halo (grid 1 input atom a = owner rank, index in the
+ * owner's home order, import shift).  A force-only DD step is then
+ *   nbx_peer_put_x (grid-0 X op + publish + signal)  -> local prune/force ->
+ *   nbx_peer_halo_x (wait + gather halo x over NVLink into grid 1) -> nonlocal prune ->
+ *   nbx_peer_force_nonlocal (j forces red.add'ed into the owners' inboxes + signal) ->
+ *   nbx_peer_get_f (wait + grid-0 F op + inbox)
+ * with one monotonically increasing `seq` per step, identical on all ranks.  Waits are
+ * bounded (env NBX_PEER_TIMEOUT_S, default 30): nbx_peer_status reports a timeout.        */
+#define NBX_PEER_HANDLE_BYTES 64
+NBX_API int nbx_peer_init(nbx_ctx* ctx, int32_t rank, int32_t world, int32_t capacity, void* handle_out);
+NBX_API int nbx_peer_open(nbx_ctx* ctx, const void* handles /* world * NBX_PEER_HANDLE_BYTES */);
+NBX_API int nbx_peer_set_halo(nbx_ctx* ctx, int32_t n_halo, const int32_t* owner_dev, const int32_t* home_dev,
+                              const float* shift_dev /* [n_halo][3] */, void* stream);
+NBX_API int nbx_peer_put_x(nbx_ctx* ctx, const float* x_home_dev, uint32_t seq, void* stream);
+NBX_API int nbx_peer_halo_x(nbx_ctx* ctx, uint32_t seq, void* stream);
+NBX_API int nbx_peer_force_nonlocal(nbx_ctx* ctx, uint32_t seq, void* stream);
+NBX_API int nbx_peer_get_f(nbx_ctx* ctx, float* f_home_dev, uint32_t seq, void* stream);
+NBX_API int nbx_peer_status(nbx_ctx* ctx, int32_t* timed_out);
+
 /* Energies and virial accumulated since the last clear.  Reads grid buffers, so call it
  * after nbx_force and BEFORE nbx_get_f.  e_host[2] = {E_lj, E_coul incl. self term},
  * virial_host[9] = -1/2 sum x (x) f - 1/2 sum s (x) fshift (row-major).  Synchronises.    */

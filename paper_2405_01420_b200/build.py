@@ -15,7 +15,7 @@ OBJ = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libnbx.so")
 ROOT = os.path.dirname(HERE)
 
-SOURCES = ["capi.cu", "grid.cu", "search.cu", "force.cu", "bufops.cu"]
+SOURCES = ["capi.cu", "grid.cu", "search.cu", "force.cu", "bufops.cu", "peer.cu"]
 HEADERS = ["nbx_internal.cuh", "pairmath.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",

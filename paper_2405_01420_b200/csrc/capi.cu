@@ -185,6 +185,7 @@ NBX_API int nbx_destroy(nbx_ctx* ctx)
     ctx->q_g.release(); ctx->type_g.release(); ctx->excl_off_g.release(); ctx->excl_gid_g.release();
     ctx->c6c12s.release(); ctx->acc.release(); ctx->sumq2.release(); ctx->counter.release();
     for (auto& g : ctx->graphs) cudaGraphExecDestroy(g.exec);
+    peer_release(ctx);
     if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
     delete ctx;
     return NBX_OK;
@@ -392,6 +393,88 @@ NBX_API int nbx_step_graph(nbx_ctx* ctx, const float* x, float* f, uint32_t what
     }
     NBX_CUDA(cudaGraphLaunch(g->exec, (cudaStream_t)stream));
     ctx->launches += g->kernels;
+    return NBX_OK;
+    NBX_GUARD_END
+}
+
+// ---- NVLink peer-memory halo (peer.cu) -------------------------------------------------
+NBX_API int nbx_peer_init(nbx_ctx* ctx, int32_t rank, int32_t world, int32_t capacity, void* handle_out)
+{
+    NBX_GUARD_BEGIN
+    NBX_CHECK_CTX(ctx);
+    if (world < 1 || rank < 0 || rank >= world || capacity < 1 || !handle_out)
+        return fail(NBX_EINVAL, "bad peer arguments");
+    peer_init(ctx, rank, world, capacity, handle_out);
+    return NBX_OK;
+    NBX_GUARD_END
+}
+
+NBX_API int nbx_peer_open(nbx_ctx* ctx, const void* handles)
+{
+    NBX_GUARD_BEGIN
+    NBX_CHECK_CTX(ctx);
+    if (!handles) return fail(NBX_EINVAL, "null handles");
+    peer_open(ctx, handles);
+    return NBX_OK;
+    NBX_GUARD_END
+}
+
+NBX_API int nbx_peer_set_halo(nbx_ctx* ctx, int32_t n_halo, const int32_t* owner, const int32_t* home,
+                              const float* shift, void* stream)
+{
+    NBX_GUARD_BEGIN
+    NBX_CHECK_CTX(ctx);
+    if (n_halo < 0 || (n_halo > 0 && (!owner || !home || !shift))) return fail(NBX_EINVAL, "bad halo map");
+    peer_set_halo(ctx, n_halo, owner, home, shift, (cudaStream_t)stream);
+    ctx->epoch++;
+    return NBX_OK;
+    NBX_GUARD_END
+}
+
+NBX_API int nbx_peer_put_x(nbx_ctx* ctx, const float* x_home, uint32_t seq, void* stream)
+{
+    NBX_GUARD_BEGIN
+    NBX_CHECK_CTX(ctx);
+    if (!x_home && ctx->grid[0].n > 0) return fail(NBX_EINVAL, "null coordinates");
+    peer_put_x(ctx, x_home, seq, (cudaStream_t)stream);
+    return NBX_OK;
+    NBX_GUARD_END
+}
+
+NBX_API int nbx_peer_halo_x(nbx_ctx* ctx, uint32_t seq, void* stream)
+{
+    NBX_GUARD_BEGIN
+    NBX_CHECK_CTX(ctx);
+    peer_halo_x(ctx, seq, (cudaStream_t)stream);
+    return NBX_OK;
+    NBX_GUARD_END
+}
+
+NBX_API int nbx_peer_force_nonlocal(nbx_ctx* ctx, uint32_t seq, void* stream)
+{
+    NBX_GUARD_BEGIN
+    NBX_CHECK_CTX(ctx);
+    peer_force_nonlocal(ctx, seq, (cudaStream_t)stream);
+    return NBX_OK;
+    NBX_GUARD_END
+}
+
+NBX_API int nbx_peer_get_f(nbx_ctx* ctx, float* f_home, uint32_t seq, void* stream)
+{
+    NBX_GUARD_BEGIN
+    NBX_CHECK_CTX(ctx);
+    if (!f_home && ctx->grid[0].n > 0) return fail(NBX_EINVAL, "null force buffer");
+    peer_get_f(ctx, f_home, seq, (cudaStream_t)stream);
+    return NBX_OK;
+    NBX_GUARD_END
+}
+
+NBX_API int nbx_peer_status(nbx_ctx* ctx, int32_t* timed_out)
+{
+    NBX_GUARD_BEGIN
+    NBX_CHECK_CTX(ctx);
+    if (!timed_out) return fail(NBX_EINVAL, "null output");
+    *timed_out = peer_status(ctx);
     return NBX_OK;
     NBX_GUARD_END
 }

@@ -91,6 +91,8 @@ struct List {
     DBuf<char> tmp;
 };
 
+struct Peer; // peer.cu: NVLink peer-memory halo state (DD, row e)
+
 struct ForceConsts {
     float epsfac, k_rf, two_k_rf, c_rf, beta, beta2, beta3, beta3_monic, sh_ewald, sh_lj6, sh_lj12, rc2, rli2;
     float fsw_r1, fsw_a6, fsw_b6, fsw_a12, fsw_b12, fsw_p6, fsw_q6, fsw_p12, fsw_q12, fsw_c6, fsw_c12;
@@ -131,6 +133,7 @@ struct nbx_ctx {
         int kernels;
         cudaGraphExec_t exec;
     };
+    nbx::Peer* peer = nullptr;
     uint64_t epoch = 1;
     std::vector<StepGraph> graphs;
     cudaStream_t cap_stream = nullptr;
@@ -166,13 +169,22 @@ void grid_build(nbx_ctx* ctx, int g, int n, const float* x, const int* gid, cons
 void search(nbx_ctx* ctx, int l, cudaStream_t st);
 void prune(nbx_ctx* ctx, int l, int part, int nparts, cudaStream_t st);
 void count_pairs(nbx_ctx* ctx, int l, long long* pairs, long long* slots, cudaStream_t st);
-void force(nbx_ctx* ctx, int l, unsigned flags, cudaStream_t st);
+void force(nbx_ctx* ctx, int l, unsigned flags, cudaStream_t st, float4* const* fj_dst = nullptr);
 void put_x(nbx_ctx* ctx, int g, const float* x, cudaStream_t st);
 void get_f(nbx_ctx* ctx, int g, float* f, int accumulate, cudaStream_t st);
 void virial_sum(nbx_ctx* ctx, int g, cudaStream_t st);
 void halo_pack_x(const float* x, const int* idx, int n, float3 shift, float* out, cudaStream_t st);
 void halo_unpack_add_f(float* f, const int* idx, int n, const float* in, cudaStream_t st);
 double fma_peak(cudaStream_t st);
+void peer_release(nbx_ctx* ctx);
+void peer_init(nbx_ctx* ctx, int rank, int world, int cap, void* handle_out);
+void peer_open(nbx_ctx* ctx, const void* handles);
+void peer_set_halo(nbx_ctx* ctx, int n, const int* owner, const int* home, const float* shift, cudaStream_t st);
+void peer_put_x(nbx_ctx* ctx, const float* x, unsigned seq, cudaStream_t st);
+void peer_halo_x(nbx_ctx* ctx, unsigned seq, cudaStream_t st);
+void peer_force_nonlocal(nbx_ctx* ctx, unsigned seq, cudaStream_t st);
+void peer_get_f(nbx_ctx* ctx, float* f, unsigned seq, cudaStream_t st);
+int peer_status(nbx_ctx* ctx);
 ForceConsts make_force_consts(const nbx_consts& c);
 
 } // namespace nbx

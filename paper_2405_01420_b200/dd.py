@@ -148,6 +148,43 @@ class NbxEngine:
     def launch_count(self):
         return self.nbx.lib().nbx_launch_count(self.ctx.h)
 
+    # -- NVLink peer-memory halo (csrc/peer.cu) ------------------------------------------
+    def peer_init(self, rank, world, capacity):
+        h = np.zeros(64, np.uint8)
+        self.nbx.check(self.nbx.lib().nbx_peer_init(self.ctx.h, rank, world, capacity, self.nbx._ptr(h)))
+        return h
+
+    def peer_open(self, handles):
+        h = np.ascontiguousarray(handles, np.uint8)
+        self.nbx.check(self.nbx.lib().nbx_peer_open(self.ctx.h, self.nbx._ptr(h)))
+
+    def peer_set_halo(self, owner, home, shift):
+        nbx = self.nbx
+        n = int(owner.shape[0])
+        nbx.check(nbx.lib().nbx_peer_set_halo(self.ctx.h, n, nbx._dev_ptr(owner) if n else None,
+                                              nbx._dev_ptr(home) if n else None,
+                                              nbx._dev_ptr(shift) if n else None, self._st()))
+
+    def peer_put_x(self, x, seq, stream=None):
+        self.nbx.check(self.nbx.lib().nbx_peer_put_x(self.ctx.h, self.nbx._dev_ptr(x) if x.shape[0] else None,
+                                                     seq, self._st(stream)))
+
+    def peer_halo_x(self, seq, stream=None):
+        self.nbx.check(self.nbx.lib().nbx_peer_halo_x(self.ctx.h, seq, self._st(stream)))
+
+    def peer_force_nonlocal(self, seq, stream=None):
+        self.nbx.check(self.nbx.lib().nbx_peer_force_nonlocal(self.ctx.h, seq, self._st(stream)))
+
+    def peer_get_f(self, f, seq, stream=None):
+        self.nbx.check(self.nbx.lib().nbx_peer_get_f(self.ctx.h, self.nbx._dev_ptr(f) if f.shape[0] else None,
+                                                     seq, self._st(stream)))
+
+    def peer_status(self):
+        import ctypes as C
+        v = C.c_int32()
+        self.nbx.check(self.nbx.lib().nbx_peer_status(self.ctx.h, C.byref(v)))
+        return v.value
+
     def fma_peak(self):
         import ctypes as C
         v = C.c_double()
@@ -163,7 +200,7 @@ class Pulse:
 class DomainDecomposition:
     """One rank of the DD NB path.  `engine` is NbxEngine (GPU) or a test double."""
 
-    def __init__(self, system, rank, world, engine_factory, device=None, group=None):
+    def __init__(self, system, rank, world, engine_factory, device=None, group=None, halo="nccl"):
         import torch
         import torch.distributed as dist
 
@@ -189,6 +226,11 @@ class DomainDecomposition:
         self.nstlist = system.nstlist
         self.prune_every = system.prune_every
         self.comm_stream = None
+        if halo not in ("nccl", "p2p"):
+            raise ValueError("halo must be 'nccl' or 'p2p'")
+        self.halo = halo  # force-only steps: NCCL pulses, or NVLink peer memory (csrc/peer.cu)
+        self.seq = 0
+        self._peer_ready = False
         self.profile_phases = False  # record per-phase CUDA events in step() (bench breakdown)
         self.phase_log = []
 
@@ -216,6 +258,8 @@ class DomainDecomposition:
         owner = cidx[:, 0] + self.dims[0] * (cidx[:, 1] + self.dims[1] * cidx[:, 2])
         home = torch.nonzero(owner == self.rank).flatten()
         self.home_gid = home.to(torch.int32)
+        if self.halo == "p2p":
+            self._owner, self._xw = owner, xw
         self.n_home = int(home.numel())
         X = xw[home].contiguous()
         G = self.home_gid.clone()
@@ -292,7 +336,44 @@ class DomainDecomposition:
         eng.search(0)
         eng.grid_build(1, self.x_ext[self.n_home:], self.gid_ext[self.n_home:], lo_n, size_n)
         eng.search(1)
+        if self.halo == "p2p":
+            self._peer_map()
         return self.n_home
+
+    def _peer_map(self):
+        """Peer halo map after a repartition: for every imported atom its owner rank, its index
+        in the owner's home order (home atoms are in increasing global id) and its import
+        shift (a multiple of the box edge per dimension)."""
+        torch, dist = self.torch, self.dist
+        dev = self.device
+        owner = self._owner
+        if not self._peer_ready:
+            cap = int(math.ceil(1.5 * self.sys.natoms / self.world)) + 4096
+            h = self.engine.peer_init(self.rank, self.world, cap)
+            ht = torch.from_numpy(h).to(dev)
+            hs = [torch.empty_like(ht) for _ in range(self.world)]
+            dist.all_gather(hs, ht, group=self.group)
+            self.engine.peer_open(torch.cat(hs).cpu().numpy())
+            self._peer_ready = True
+        hidx = torch.empty_like(owner)
+        for r in range(self.world):
+            m = torch.nonzero(owner == r).flatten()
+            hidx[m] = torch.arange(m.numel(), device=dev)
+        g = self.gid_ext[self.n_home:].long()
+        box = torch.tensor(self.box, dtype=torch.float32, device=dev)
+        sh = torch.round((self.x_ext[self.n_home:] - self._xw[g]) / box) * box
+        self._peer_owner = owner[g].to(torch.int32).contiguous()
+        self._peer_home = hidx[g].to(torch.int32).contiguous()
+        self._peer_shift = sh.to(torch.float32).contiguous()
+        self.engine.peer_set_halo(self._peer_owner, self._peer_home, self._peer_shift)
+        self._owner = self._xw = None
+        # every rank's map and regions are in place before anyone's next signal
+        dist.barrier(group=self.group)
+
+    def check_peer(self):
+        """Raise if a peer-memory wait timed out (a rank stopped taking steps)."""
+        if self.halo == "p2p" and self._peer_ready and self.engine.peer_status():
+            raise RuntimeError("peer-memory halo: a wait for another rank timed out")
 
     # ---------------------------------------------------------------------- per step
     def halo_x(self):
@@ -328,10 +409,12 @@ class DomainDecomposition:
         the next step) and, with energy/virial, the all-reduced (energies, virial)."""
         eng = self.engine
         ev = self._events() if self.profile_phases else None
-        if x_home is not None:
-            self.x_ext[:self.n_home].copy_(x_home)
         if prune is None:
             prune = bool(self.prune_every) and step % self.prune_every == 0
+        if self.halo == "p2p" and not (energy or virial):
+            return self._step_p2p(x_home, prune, ev)
+        if x_home is not None:
+            self.x_ext[:self.n_home].copy_(x_home)
         if ev:
             ev[0].record()
         works = self.halo_x()  # NCCL in flight while the local kernel runs
@@ -370,6 +453,37 @@ class DomainDecomposition:
         f_home = self.f_ext[:self.n_home]
         return (f_home, res) if res is not None else f_home
 
+    def _step_p2p(self, x_home, prune, ev):
+        """Force-only step with the NVLink peer-memory halo: no messages, no pack/unpack, no
+        reverse pulses (csrc/peer.cu).  x_home=None: the coordinates of the last repartition
+        (or of the last NCCL-path step)."""
+        eng = self.engine
+        self.seq += 1
+        seq = self.seq & 0xFFFFFFFF
+        x = self.x_ext[:self.n_home] if x_home is None else x_home.contiguous()
+        if ev:
+            ev[0].record()
+        eng.peer_put_x(x, seq)  # grid-0 X op + publish + signal
+        if prune:
+            eng.prune(0)
+        eng.force(0, 0)
+        if ev:
+            ev[1].record()
+        eng.peer_halo_x(seq)  # wait for the owners, gather the halo over NVLink
+        if ev:
+            ev[2].record()
+        if prune:
+            eng.prune(1)
+        eng.peer_force_nonlocal(seq)  # j forces straight into the owners' inboxes
+        if ev:
+            ev[3].record()
+        f_home = self.f_ext[:self.n_home]
+        eng.peer_get_f(f_home, seq)  # wait for the senders, home forces + inbox
+        if ev:
+            ev[4].record()
+            self.phase_log.append(ev)
+        return f_home
+
     def _events(self):
         E = self.torch.cuda.Event
         return [E(enable_timing=True) for _ in range(5)]
@@ -406,7 +520,8 @@ def bench(args, METRIC, UNIT, FLOPS_PER_PAIR, DESC, ClockSampler, time_cpu_port,
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     s = systems.make(args.config)
-    dd = DomainDecomposition(s, rank, world, lambda sy, pbc: NbxEngine(sy, local, pbc), device=dev)
+    halo = os.environ.get("NBX_DD_HALO", "p2p")
+    dd = DomainDecomposition(s, rank, world, lambda sy, pbc: NbxEngine(sy, local, pbc), device=dev, halo=halo)
     xg = torch.from_numpy(s.x).to(dev)
     peak = dd.engine.fma_peak()
     dd.repartition(xg)  # setup: first search sizes the lists and the single-pass buffers
@@ -447,6 +562,7 @@ def bench(args, METRIC, UNIT, FLOPS_PER_PAIR, DESC, ClockSampler, time_cpu_port,
     e1.record(st)
     torch.cuda.synchronize()
     dist.barrier()
+    dd.check_peer()
     launches = dd.engine.launch_count() - l0
     ms = e0.elapsed_time(e1)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -470,7 +586,9 @@ def bench(args, METRIC, UNIT, FLOPS_PER_PAIR, DESC, ClockSampler, time_cpu_port,
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"{args.config}: {DESC[args.config]}", "natoms": s.natoms,
-                       "parallelism": f"spatial DD {dd.dims[0]}x{dd.dims[1]}x{dd.dims[2]}, NCCL P2P halo",
+                       "parallelism": f"spatial DD {dd.dims[0]}x{dd.dims[1]}x{dd.dims[2]}, "
+                       + ("NVLink peer-memory halo (fused into X op / nonlocal force / F op)" if halo == "p2p"
+                          else "NCCL P2P halo"),
                        "nstlist": s.nstlist, "prune_every": s.prune_every,
                        "l2": "inputs larger than L2" if s.natoms > 2_000_000 else "per-rank inputs may fit L2"},
             "steps_per_s": 1e3 / ms_per_step, "ns_per_day": 86.4 * s.dt_fs / ms_per_step,

@@ -66,7 +66,9 @@ EXPORTS = ["nbx_last_error", "nbx_version", "nbx_derive_consts", "nbx_create", "
            "nbx_set_topology", "nbx_set_box", "nbx_grid_build", "nbx_search", "nbx_put_x",
            "nbx_prune", "nbx_force", "nbx_get_f", "nbx_step_graph", "nbx_energies", "nbx_clear_energies",
            "nbx_grid_info_get", "nbx_grid_export", "nbx_list_sizes_get", "nbx_list_export",
-           "nbx_count_pairs", "nbx_fma_peak", "nbx_launch_count", "nbx_halo_pack_x", "nbx_halo_unpack_add_f"]
+           "nbx_count_pairs", "nbx_fma_peak", "nbx_launch_count", "nbx_halo_pack_x", "nbx_halo_unpack_add_f",
+           "nbx_peer_init", "nbx_peer_open", "nbx_peer_set_halo", "nbx_peer_put_x", "nbx_peer_halo_x",
+           "nbx_peer_force_nonlocal", "nbx_peer_get_f", "nbx_peer_status"]
 
 _lib = None
 
@@ -106,6 +108,14 @@ def lib():
         L.nbx_launch_count.restype = C.c_int64
         L.nbx_halo_pack_x.argtypes = [vp, vp, i32, vp, vp, vp]
         L.nbx_halo_unpack_add_f.argtypes = [vp, vp, i32, vp, vp]
+        L.nbx_peer_init.argtypes = [vp, i32, i32, i32, vp]
+        L.nbx_peer_open.argtypes = [vp, vp]
+        L.nbx_peer_set_halo.argtypes = [vp, i32, vp, vp, vp, vp]
+        L.nbx_peer_put_x.argtypes = [vp, vp, u32, vp]
+        L.nbx_peer_halo_x.argtypes = [vp, u32, vp]
+        L.nbx_peer_force_nonlocal.argtypes = [vp, u32, vp]
+        L.nbx_peer_get_f.argtypes = [vp, vp, u32, vp]
+        L.nbx_peer_status.argtypes = [vp, vp]
         _lib = L
     return _lib
 

@@ -23,8 +23,10 @@ def _ngpu():
     return torch.cuda.device_count()
 
 
+@pytest.mark.parametrize("halo", ["nccl", "p2p"])
 @pytest.mark.parametrize("world", [2, 4, 8])
-def test_dd_nccl_matches_single_gpu(gpu, world):
+def test_dd_matches_single_gpu(gpu, world, halo):
+    """halo=p2p: force-only steps through the NVLink peer-memory halo (csrc/peer.cu)."""
     if _ngpu() < world:
         pytest.skip(f"needs {world} GPUs")
     natoms = 150000 if world < 8 else 300000
@@ -32,7 +34,7 @@ def test_dd_nccl_matches_single_gpu(gpu, world):
         out = os.path.join(tmp, "dd.npz")
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
                "--master-addr", "127.0.0.1", "--master-port", str(29500 + world),
-               os.path.join(ROOT, "tests", "dd_gpu_worker.py"), "water12m", str(natoms), out]
+               os.path.join(ROOT, "tests", "dd_gpu_worker.py"), "water12m", str(natoms), out, halo]
         r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
         assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
         d = np.load(out)
@@ -43,3 +45,6 @@ def test_dd_nccl_matches_single_gpu(gpu, world):
     assert_forces(d["f2"], d["f2_ref"])
     assert_energies(d["e2"], d["e2_ref"])
     assert_virial(d["vir2"], d["vir2_ref"])
+    assert_forces(d["fa"], d["f_ref"])
+    assert_forces(d["fb"], d["f2_ref"])
+    assert_forces(d["fb2"], d["f2_ref"])
