@@ -231,6 +231,8 @@ class DomainDecomposition:
         self.halo = halo  # force-only steps: NCCL pulses, or NVLink peer memory (csrc/peer.cu)
         self.seq = 0
         self._peer_ready = False
+        self.timing = None  # dict: host-side section times of repartition (tools/dd_repart_timing.py)
+        self._t_last = 0.0
         self.profile_phases = False  # record per-phase CUDA events in step() (bench breakdown)
         self.phase_log = []
 
@@ -244,10 +246,20 @@ class DomainDecomposition:
             return []
         return dist.batch_isend_irecv(ops)
 
+    def _tick(self, name=None):
+        if self.timing is None:
+            return
+        self.torch.cuda.synchronize()
+        t = time.perf_counter()
+        if name is not None:
+            self.timing[name] = self.timing.get(name, 0.0) + (t - self._t_last)
+        self._t_last = t
+
     def repartition(self, x_global):
         """Assign home atoms, build the halo plan, grids and lists (a search step)."""
         torch = self.torch
         dev = self.device
+        self._tick()
         box = torch.tensor(self.box, dtype=torch.float32, device=dev)
         xg = x_global.to(dev, torch.float32)
         xw = xg - torch.floor(xg / box) * box
@@ -259,10 +271,14 @@ class DomainDecomposition:
         home = torch.nonzero(owner == self.rank).flatten()
         self.home_gid = home.to(torch.int32)
         if self.halo == "p2p":
-            self._owner, self._xw = owner, xw
+            self._xw = xw
+        self._tick("owners")
         self.n_home = int(home.numel())
         X = xw[home].contiguous()
-        G = self.home_gid.clone()
+        # per atom (global id, owner rank, index in the owner's home order), carried through
+        # the pulses with the coordinates (the peer-memory halo addresses owners by it)
+        M = torch.stack([self.home_gid, torch.full_like(self.home_gid, self.rank),
+                         torch.arange(self.n_home, dtype=torch.int32, device=dev)], dim=1)
         lo = np.array([self.coord[d] * self.D[d] for d in range(3)])
         self.lo = lo
         self.pulses = []
@@ -306,20 +322,22 @@ class DomainDecomposition:
             send_u = (X[p.up_idx.long()] + torch.from_numpy(su).to(dev)).contiguous()
             recv_u = torch.empty((p.n_from_up, 3), dtype=torch.float32, device=dev)
             recv_d = torch.empty((p.n_from_down, 3), dtype=torch.float32, device=dev)
-            gsd, gsu = G[p.down_idx.long()].contiguous(), G[p.up_idx.long()].contiguous()
-            gru = torch.empty(p.n_from_up, dtype=torch.int32, device=dev)
-            grd = torch.empty(p.n_from_down, dtype=torch.int32, device=dev)
+            gsd, gsu = M[p.down_idx.long()].contiguous(), M[p.up_idx.long()].contiguous()
+            gru = torch.empty((p.n_from_up, 3), dtype=torch.int32, device=dev)
+            grd = torch.empty((p.n_from_down, 3), dtype=torch.int32, device=dev)
             for w in self._exchange([(send_d, p.down_peer), (send_u, p.up_peer), (gsd, p.down_peer),
                                      (gsu, p.up_peer)],
                                     [(recv_u, p.up_peer), (recv_d, p.down_peer), (gru, p.up_peer),
                                      (grd, p.down_peer)]):
                 w.wait()
             X = torch.cat([X, recv_u, recv_d])
-            G = torch.cat([G, gru, grd])
+            M = torch.cat([M, gru, grd])
             self.pulses.append(p)
+            self._tick(f"pulse{d}")
         self.n_ext = X.shape[0]
         self.x_ext = X.contiguous()
-        self.gid_ext = G.contiguous()
+        self.gid_ext = M[:, 0].contiguous()
+        self._meta_halo = M[self.n_home:]
         self.f_ext = torch.zeros_like(self.x_ext)
         self.fbuf_down = [torch.empty((p.down_idx.numel(), 3), dtype=torch.float32, device=dev) for p in self.pulses]
         self.fbuf_up = [torch.empty((p.up_idx.numel(), 3), dtype=torch.float32, device=dev) for p in self.pulses]
@@ -332,12 +350,18 @@ class DomainDecomposition:
         size_n = np.array([self.D[d] + 2 * self.rl if self.dims[d] > 1 else self.box[d] for d in range(3)], np.float32)
         lo_n = np.array([lo[d] - self.rl if self.dims[d] > 1 else 0.0 for d in range(3)], np.float32)
         eng = self.engine
+        self._tick("buffers")
         eng.grid_build(0, self.x_ext[:self.n_home], self.gid_ext[:self.n_home], lo_l, size_l)
+        self._tick("grid0")
         eng.search(0)
+        self._tick("search0")
         eng.grid_build(1, self.x_ext[self.n_home:], self.gid_ext[self.n_home:], lo_n, size_n)
+        self._tick("grid1")
         eng.search(1)
+        self._tick("search1")
         if self.halo == "p2p":
             self._peer_map()
+            self._tick("peer_map")
         return self.n_home
 
     def _peer_map(self):
@@ -346,7 +370,6 @@ class DomainDecomposition:
         shift (a multiple of the box edge per dimension)."""
         torch, dist = self.torch, self.dist
         dev = self.device
-        owner = self._owner
         if not self._peer_ready:
             cap = int(math.ceil(1.5 * self.sys.natoms / self.world)) + 4096
             h = self.engine.peer_init(self.rank, self.world, cap)
@@ -355,18 +378,14 @@ class DomainDecomposition:
             dist.all_gather(hs, ht, group=self.group)
             self.engine.peer_open(torch.cat(hs).cpu().numpy())
             self._peer_ready = True
-        hidx = torch.empty_like(owner)
-        for r in range(self.world):
-            m = torch.nonzero(owner == r).flatten()
-            hidx[m] = torch.arange(m.numel(), device=dev)
-        g = self.gid_ext[self.n_home:].long()
+        m = self._meta_halo
         box = torch.tensor(self.box, dtype=torch.float32, device=dev)
-        sh = torch.round((self.x_ext[self.n_home:] - self._xw[g]) / box) * box
-        self._peer_owner = owner[g].to(torch.int32).contiguous()
-        self._peer_home = hidx[g].to(torch.int32).contiguous()
+        sh = torch.round((self.x_ext[self.n_home:] - self._xw[m[:, 0].long()]) / box) * box
+        self._peer_owner = m[:, 1].contiguous()
+        self._peer_home = m[:, 2].contiguous()
         self._peer_shift = sh.to(torch.float32).contiguous()
         self.engine.peer_set_halo(self._peer_owner, self._peer_home, self._peer_shift)
-        self._owner = self._xw = None
+        self._xw = None
         # every rank's map and regions are in place before anyone's next signal
         dist.barrier(group=self.group)
 
