@@ -6,6 +6,7 @@
 // into 2 x 2 x (2 x 4): halves of 16, j-clusters of 8, i-clusters of 4.
 // Every floating-point operation that decides a bin or a slot is the exact op sequence of the
 // CPU oracle (oracle/nbx_oracle.c ora_grid_build), so the layout is bit-identical.
+#include <algorithm>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
@@ -47,16 +48,22 @@ __device__ __forceinline__ float3 wrap_atom(const float* x, int a, const BinArgs
 
 __global__ void k_bin(BinArgs A, unsigned long long* key, int* val, int* col_count)
 {
-    int a = blockIdx.x * blockDim.x + threadIdx.x;
-    if (a >= A.n) return;
-    float3 k;
-    float3 w = wrap_atom(A.x, a, A, k);
-    int cx = cell_index(w.x, A.lo.x, A.inv_cell[0], A.ncx);
-    int cy = cell_index(w.y, A.lo.y, A.inv_cell[1], A.ncy);
-    int col = cx * A.ncy + cy;
-    key[a] = ((unsigned long long)(unsigned)col << 32) | ordkey(w.z);
-    val[a] = a;
-    atomicAdd(&col_count[col], 1);
+    const int a = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool real = a < A.n;
+    int col = -1;
+    if (real) {
+        float3 k;
+        float3 w = wrap_atom(A.x, a, A, k);
+        int cx = cell_index(w.x, A.lo.x, A.inv_cell[0], A.ncx);
+        int cy = cell_index(w.y, A.lo.y, A.inv_cell[1], A.ncy);
+        col = cx * A.ncy + cy;
+        key[a] = ((unsigned long long)(unsigned)col << 32) | ordkey(w.z);
+        val[a] = a;
+    }
+    // warp-aggregated column counts: consecutive input atoms (molecules, lattice rows) mostly
+    // share a column, so one atomic per distinct column per warp instead of one per atom
+    const unsigned peers = __match_any_sync(0xffffffffu, col);
+    if (real && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&col_count[col], __popc(peers));
 }
 
 __global__ void k_pad(const int* col_count, int ncol, int* padded)
@@ -176,37 +183,46 @@ __device__ __forceinline__ void bb_reduce(float3& lo, float3& hi, int& nr, int x
     }
 }
 
+// grid-stride over super-clusters, one warp each; the fp64 sum of q^2 (self energy) is kept
+// per warp and reduced per block, so there is one global atomic per block, not per sci
 __global__ void k_bbox(BBArgs A, int gslot)
 {
+    __shared__ double s_q2;
     const int lane = threadIdx.x & 31;
-    const int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (s >= A.nsci) return;
-    const int slot = 32 * s + lane;
-    const bool real = A.order[slot] >= 0;
-    float4 x = A.xq[slot];
-    float3 lo = real ? make_float3(x.x, x.y, x.z) : make_float3(NBX_BB_EMPTY, NBX_BB_EMPTY, NBX_BB_EMPTY);
-    float3 hi = real ? make_float3(x.x, x.y, x.z) : make_float3(-NBX_BB_EMPTY, -NBX_BB_EMPTY, -NBX_BB_EMPTY);
-    int nr = real ? 1 : 0;
-    double q2 = real ? (double)x.w * (double)x.w : 0.0;
-    bb_reduce(lo, hi, nr, 1, 2);
-    if ((lane & 3) == 0) {
-        int ci = 8 * s + (lane >> 2);
-        A.bb_ci[2 * ci] = make_float4(lo.x, lo.y, lo.z, (float)nr);
-        A.bb_ci[2 * ci + 1] = make_float4(hi.x, hi.y, hi.z, 0.f);
+    if (threadIdx.x == 0) s_q2 = 0.0;
+    __syncthreads();
+    double q2w = 0.0;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    for (int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < A.nsci; s += nw) {
+        const int slot = 32 * s + lane;
+        const bool real = A.order[slot] >= 0;
+        float4 x = A.xq[slot];
+        float3 lo = real ? make_float3(x.x, x.y, x.z) : make_float3(NBX_BB_EMPTY, NBX_BB_EMPTY, NBX_BB_EMPTY);
+        float3 hi = real ? make_float3(x.x, x.y, x.z) : make_float3(-NBX_BB_EMPTY, -NBX_BB_EMPTY, -NBX_BB_EMPTY);
+        int nr = real ? 1 : 0;
+        q2w += real ? (double)x.w * (double)x.w : 0.0;
+        bb_reduce(lo, hi, nr, 1, 2);
+        if ((lane & 3) == 0) {
+            int ci = 8 * s + (lane >> 2);
+            A.bb_ci[2 * ci] = make_float4(lo.x, lo.y, lo.z, (float)nr);
+            A.bb_ci[2 * ci + 1] = make_float4(hi.x, hi.y, hi.z, 0.f);
+        }
+        bb_reduce(lo, hi, nr, 4, 4);
+        if ((lane & 7) == 0) {
+            int cj = 4 * s + (lane >> 3);
+            A.bb_cj[2 * cj] = make_float4(lo.x, lo.y, lo.z, (float)nr);
+            A.bb_cj[2 * cj + 1] = make_float4(hi.x, hi.y, hi.z, 0.f);
+        }
+        bb_reduce(lo, hi, nr, 8, 16);
+        if (lane == 0) {
+            A.bb_sci[2 * s] = make_float4(lo.x, lo.y, lo.z, (float)nr);
+            A.bb_sci[2 * s + 1] = make_float4(hi.x, hi.y, hi.z, 0.f);
+        }
     }
-    bb_reduce(lo, hi, nr, 4, 4);
-    if ((lane & 7) == 0) {
-        int cj = 4 * s + (lane >> 3);
-        A.bb_cj[2 * cj] = make_float4(lo.x, lo.y, lo.z, (float)nr);
-        A.bb_cj[2 * cj + 1] = make_float4(hi.x, hi.y, hi.z, 0.f);
-    }
-    bb_reduce(lo, hi, nr, 8, 16);
-    for (int o = 16; o > 0; o >>= 1) q2 += __shfl_xor_sync(0xffffffffu, q2, o);
-    if (lane == 0) {
-        A.bb_sci[2 * s] = make_float4(lo.x, lo.y, lo.z, (float)nr);
-        A.bb_sci[2 * s + 1] = make_float4(hi.x, hi.y, hi.z, 0.f);
-        atomicAdd(&A.sumq2[gslot], q2);
-    }
+    for (int o = 16; o > 0; o >>= 1) q2w += __shfl_xor_sync(0xffffffffu, q2w, o);
+    if (lane == 0) atomicAdd(&s_q2, q2w);
+    __syncthreads();
+    if (threadIdx.x == 0) atomicAdd(&A.sumq2[gslot], s_q2);
 }
 
 // x-y bounding box of every column (union of its slab boxes), for the search's exact
@@ -348,7 +364,8 @@ void grid_build(nbx_ctx* ctx, int g, int n, const float* x, const int* gid, cons
         BA.bb_cj = G.bb_cj.p;
         BA.bb_sci = G.bb_sci.p;
         BA.sumq2 = ctx->sumq2.p;
-        k_bbox<<<blocks, threads, 0, st>>>(BA, g);
+        const int bblocks = std::min(blocks, ctx->num_sms * 16);
+        k_bbox<<<bblocks, threads, 0, st>>>(BA, g);
         ctx->launches++;
         NBX_CUDA(cudaGetLastError());
     }
