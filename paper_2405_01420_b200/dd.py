@@ -596,6 +596,34 @@ def bench(args, METRIC, UNIT, FLOPS_PER_PAIR, DESC, ClockSampler, time_cpu_port,
         dd.step(x_home, step=1)
     phases = dd.phase_summary()
     dd.profile_phases = False
+    # e2e: every step copies this rank's home coordinates from pinned host memory and reads
+    # its home forces back (the public DomainDecomposition.step API; no search steps)
+    e2e = None
+    if not args.no_e2e:
+        xh = x_home.cpu().pin_memory()
+        fh = torch.empty((dd.n_home, 3), dtype=torch.float32).pin_memory()
+        xd = torch.empty_like(x_home)
+        Ke = max(1, min(K, 50))
+        dist.barrier()
+        torch.cuda.synchronize()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(st)
+        for k in range(Ke):
+            xd.copy_(xh, non_blocking=True)
+            fo = dd.step(xd, step=1 + k)
+            fh.copy_(fo, non_blocking=True)
+        a1.record(st)
+        torch.cuda.synchronize()
+        dd.check_peer()
+        te = torch.tensor([a0.elapsed_time(a1)], dtype=torch.float64, device=dev)
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        nb = torch.tensor([xh.numel() * 4, fh.numel() * 4], dtype=torch.float64, device=dev)
+        dist.all_reduce(nb)
+        e2e = {"value": pairs_tot * Ke / (float(te[0]) * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": int(nb[0]), "d2h_bytes_per_step": int(nb[1]), "steps": Ke,
+               "ms_per_step": float(te[0]) / Ke,
+               "api": "paper_2405_01420_b200.dd.DomainDecomposition.step (ctypes -> libnbx.so C-ABI), "
+                      "all ranks, max over ranks"}
     if rank == 0:
         ms_per_step = ms_max / K
         value = pairs_tot * K / (ms_max * 1e-3)
@@ -615,7 +643,7 @@ def bench(args, METRIC, UNIT, FLOPS_PER_PAIR, DESC, ClockSampler, time_cpu_port,
             "roofline": {"bound": "fp32", "achieved": value / 1e12 * fl / world, "peak": peak, "unit": "TFLOP/s",
                          "frac": value / 1e12 * fl / world / peak, "traffic": load_traffic(args.config, world),
                          "note": "per GPU, whole NB step (not kernel-only) at N>1"},
-            "e2e": None, "gpu_launches": int(launches), "clocks": clk, "searches": n_search,
+            "e2e": e2e, "gpu_launches": int(launches), "clocks": clk, "searches": n_search,
             "dd_phases_ms_rank0": phases,
             "step_ms_rank0": {"median": step_ms[K // 2], "max": step_ms[-1], "search_steps": search_ms},
         }
