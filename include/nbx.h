@@ -43,13 +43,16 @@ typedef enum {
 } nbx_status;
 
 /* ---- parameters (mirrors the reference's per-system knobs, presets.py:28-49) ------------ */
-enum { NBX_COULOMB_RF = 0, NBX_COULOMB_EWALD = 1 };
+/* EWALD_TAB: Ewald real space with the long-range correction force (and, in energy kernels,
+ * potential) linearly interpolated from a uniform table in r instead of the fitted rational:
+ * the paper's kernel flavour for both its benchmarks. */
+enum { NBX_COULOMB_RF = 0, NBX_COULOMB_EWALD = 1, NBX_COULOMB_EWALD_TAB = 2 };
 /* LJ modifiers: potential shift (default) or force switch between rvdw_switch and rc
  * (the CHARMM/STMV flavour of the paper) */
 enum { NBX_LJ_POT_SHIFT = 0, NBX_LJ_FORCE_SWITCH = 1 };
 
 typedef struct nbx_params {
-    int32_t coulomb_type; /* NBX_COULOMB_RF or NBX_COULOMB_EWALD                           */
+    int32_t coulomb_type; /* NBX_COULOMB_RF, NBX_COULOMB_EWALD or NBX_COULOMB_EWALD_TAB     */
     float rc;             /* common LJ/Coulomb cut-off (presets.py:40 cutoff_nm)           */
     float rlist_outer;    /* pair-search radius, list lifetime nstlist (presets.py:44)     */
     float rlist_inner;    /* dynamic-prune radius, lifetime prune_every (presets.py:45)    */
@@ -79,6 +82,12 @@ typedef struct nbx_consts {
     float fsw_a6, fsw_b6, fsw_a12, fsw_b12;   /* A_a / a, B_a / a  (tables hold a * c_a)     */
     float fsw_p6, fsw_q6, fsw_p12, fsw_q12;   /* A_a / 3, B_a / 4                            */
     float fsw_c6, fsw_c12;                    /* C_a                                          */
+    /* EWALD_TAB: nodes r_k = k / tab_scale, k < tab_n; tab_scale = max(400 beta, 600) /nm,
+     * tab_n = ceil(rc tab_scale) + 2.  Force table F_k = beta^3 G(beta^2 r_k^2) (the
+     * correction in F/r = qq (r^-3 - F(r))), potential table V_k = erf(beta r_k) / r_k, each
+     * stored as (value, next - value) pairs (nbx_ewald_table).                             */
+    float tab_scale;
+    int32_t tab_n;
 } nbx_consts;
 
 /* ---- pair-list format ----------------------------------------
@@ -122,6 +131,8 @@ NBX_API const char* nbx_version(void);
 
 /* Derive the constants of a parameter set (no device needed).                           */
 NBX_API int nbx_derive_consts(const nbx_params* p, nbx_consts* out);
+/* EWALD_TAB tables for derived constants c: ftab[2 * tab_n] and vtab[2 * tab_n] (host). */
+NBX_API int nbx_ewald_table(const nbx_consts* c, float* ftab, float* vtab);
 
 /* Create a context on `device` (must be sm_100).  Replaces the reference's per-rank device
  * construction (_RankBuild -> Device/RankRuntime, runtime.py:255-304).                   */

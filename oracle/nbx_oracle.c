@@ -51,9 +51,14 @@ int ora_derive_consts(const nbx_params* p, nbx_consts* c)
               / ((2.0 * (double)p->epsilon_rf + (double)p->epsilon_r) * rc * rc * rc);
     c->k_rf = (float)krf;
     c->c_rf = (float)(1.0 / rc + krf * rc * rc);
-    double beta = (p->coulomb_type == NBX_COULOMB_EWALD) ? ewald_beta(rc, p->ewald_rtol) : 0.0;
+    const int ew = p->coulomb_type == NBX_COULOMB_EWALD || p->coulomb_type == NBX_COULOMB_EWALD_TAB;
+    double beta = ew ? ewald_beta(rc, p->ewald_rtol) : 0.0;
     c->beta = (float)beta;
-    c->sh_ewald = (p->coulomb_type == NBX_COULOMB_EWALD) ? (float)(erfc(beta * rc) / rc) : 0.0f;
+    c->sh_ewald = ew ? (float)(erfc(beta * rc) / rc) : 0.0f;
+    if (p->coulomb_type == NBX_COULOMB_EWALD_TAB) {
+        c->tab_scale = (float)(400.0 * beta > 600.0 ? 400.0 * beta : 600.0);
+        c->tab_n = (int32_t)ceil(rc * (double)c->tab_scale) + 2;
+    }
     c->sh_lj6 = (float)(1.0 / (rc * rc * rc * rc * rc * rc));
     c->sh_lj12 = (float)(1.0 / (rc * rc * rc * rc * rc * rc * rc * rc * rc * rc * rc * rc));
     c->rc2 = (float)(rc * rc);
@@ -86,11 +91,57 @@ int ora_derive_consts(const nbx_params* p, nbx_consts* c)
     return 0;
 }
 
+/* beta^3 G(beta^2 r^2) = (erf(beta r)/r - 2 beta/sqrt(pi) exp(-beta^2 r^2)) / r^2, with its
+ * series (2 beta^3/sqrt(pi)) (2/3 - 2z/5 + z^2/7 - z^3/27 + z^4/132) below z = 1e-2 */
+static double ewald_fcorr(double beta, double r)
+{
+    const double z = beta * beta * r * r, b3 = beta * beta * beta, tsp = 2.0 / sqrt(M_PI);
+    if (z < 1e-2) return tsp * b3 * (2.0 / 3.0 + z * (-2.0 / 5.0 + z * (1.0 / 7.0 + z * (-1.0 / 27.0 + z / 132.0))));
+    return (erf(beta * r) / r - tsp * beta * exp(-z)) / (r * r);
+}
+
+static double ewald_vcorr(double beta, double r)
+{
+    if (r == 0.0) return 2.0 * beta / sqrt(M_PI);
+    return erf(beta * r) / r;
+}
+
+int ora_ewald_table(const nbx_consts* c, float* ftab, float* vtab)
+{
+    const int n = c->tab_n;
+    if (n < 2 || !(c->tab_scale > 0.0f)) return 1;
+    const double beta = c->beta, h = 1.0 / (double)c->tab_scale;
+    for (int k = 0; k < n; k++) {
+        ftab[2 * k] = (float)ewald_fcorr(beta, k * h);
+        vtab[2 * k] = (float)ewald_vcorr(beta, k * h);
+    }
+    for (int k = 0; k < n; k++) {
+        ftab[2 * k + 1] = (k + 1 < n) ? ftab[2 * k + 2] - ftab[2 * k] : 0.0f;
+        vtab[2 * k + 1] = (k + 1 < n) ? vtab[2 * k + 2] - vtab[2 * k] : 0.0f;
+    }
+    return 0;
+}
+
+/* linear interpolation of a (value, difference) table at r = r2 * rinv, identical op
+ * sequence to tab_lookup() in paper_2405_01420_b200/csrc/pairmath.cuh: the floor comes from
+ * adding 2^23 - 1/2 (exact for rs >= 1/2, which R2MIN and tab_scale >= 600 guarantee) */
+static inline float tab_interp(const float* tab, float r2, float rinv, const nbx_consts* c)
+{
+    const float r2c = fminf(r2, c->rc2);
+    const float rs = r2c * (rinv * c->tab_scale);
+    const float t = rs + 8388607.5f;
+    uint32_t tb;
+    memcpy(&tb, &t, 4);
+    const int idx = (int)(tb - 0x4B000000u);
+    const float fr = rs - (t - 8388608.0f);
+    return fmaf(fr, tab[2 * idx + 1], tab[2 * idx]);
+}
+
 double ora_self_energy(const nbx_params* p, double sumq2)
 {
     nbx_consts c;
     ora_derive_consts(p, &c);
-    if (p->coulomb_type == NBX_COULOMB_EWALD)
+    if (p->coulomb_type == NBX_COULOMB_EWALD || p->coulomb_type == NBX_COULOMB_EWALD_TAB)
         return -(double)c.epsfac * sumq2 * (double)c.beta / sqrt(M_PI);
     return -0.5 * (double)c.epsfac * (double)c.c_rf * sumq2;
 }
@@ -690,7 +741,7 @@ typedef struct {
  * exclusion-correction (corrb) bits, unmasked tiles have intb = 1, corrb = 0. */
 static inline pairres pair_eval(float dx, float dy, float dz, int masked, int intb, int corrb,
                                 float qi, float qj, float c6, float c12, const nbx_consts* c,
-                                int coul, int energy, int ljmod)
+                                int coul, int energy, int ljmod, const float* ftab, const float* vtab)
 {
     pairres r = {0.0f, 0.0f, 0.0f, 0};
     float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
@@ -708,6 +759,8 @@ static inline pairres pair_eval(float dx, float dy, float dz, int masked, int in
     float fc, z = 0.0f;
     if (coul == NBX_COULOMB_RF) {
         fc = qq * fmaf(fint, rinv3, -(c->k_rf * 2.0f));
+    } else if (coul == NBX_COULOMB_EWALD_TAB) {
+        fc = qq * (fint * rinv3 - tab_interp(ftab, r2, rinv, c));
     } else {
         float beta2 = c->beta * c->beta;
         z = beta2 * r2;
@@ -738,6 +791,8 @@ static inline pairres pair_eval(float dx, float dy, float dz, int masked, int in
         r.vlj = vlj * fint;
         if (coul == NBX_COULOMB_RF)
             r.vc = qq * fmaf(c->k_rf, r2, fmaf(fint, rinv, -c->c_rf));
+        else if (coul == NBX_COULOMB_EWALD_TAB)
+            r.vc = qq * fmaf(fint, rinv - c->sh_ewald, -tab_interp(vtab, r2, rinv, c));
         else
             r.vc = qq * fmaf(fint, rinv - c->sh_ewald, -(c->beta * ora_ewald_H(z)));
     }
@@ -753,6 +808,13 @@ void ora_force(int n_sci, const nbx_sci_entry* sci, const nbx_cj_entry* cj,
     nbx_consts c;
     ora_derive_consts(p, &c);
     const int coul = p->coulomb_type, energy = (flags & NBX_FORCE_ENERGY) != 0, ljmod = p->lj_modifier;
+    float* ftab = NULL;
+    float* vtab = NULL;
+    if (coul == NBX_COULOMB_EWALD_TAB) {
+        ftab = (float*)malloc(sizeof(float) * 2 * (size_t)c.tab_n);
+        vtab = (float*)malloc(sizeof(float) * 2 * (size_t)c.tab_n);
+        ora_ewald_table(&c, ftab, vtab);
+    }
     double elj = 0.0, ec = 0.0;
     double fsh[NBX_NSHIFT * 3];
     memset(fsh, 0, sizeof(fsh));
@@ -793,7 +855,7 @@ void ora_force(int n_sci, const nbx_sci_entry* sci, const nbx_cj_entry* cj,
                             const float* cc = c6c12 + 2 * (ti * ntypes + type_j[b]);
                             float c6 = 6.0f * cc[0], c12 = 12.0f * cc[1];
                             pairres r = pair_eval(dx, dy, dz, masked, (im >> bit) & 1, (cm >> bit) & 1,
-                                                  qi, xb[3], c6, c12, &c, coul, energy, ljmod);
+                                                  qi, xb[3], c6, c12, &c, coul, energy, ljmod, ftab, vtab);
                             if (!r.valid) continue;
                             float fx = r.fscal * dx, fy = r.fscal * dy, fz = r.fscal * dz;
                             f_i[3 * a + 0] += fx; f_i[3 * a + 1] += fy; f_i[3 * a + 2] += fz;
@@ -859,7 +921,7 @@ void ora_force(int n_sci, const nbx_sci_entry* sci, const nbx_cj_entry* cj,
                                 const float* cc = c6c12 + 2 * (ti * ntypes + type_j[b]);
                                 float c6 = 6.0f * cc[0], c12 = 12.0f * cc[1];
                                 pairres r = pair_eval(dx, dy, dz, masked, (im >> bit) & 1, (cm >> bit) & 1,
-                                                      qi, xb[3], c6, c12, &c, coul, energy, ljmod);
+                                                      qi, xb[3], c6, c12, &c, coul, energy, ljmod, ftab, vtab);
                                 if (!r.valid) continue;
                                 float fx = r.fscal * dx, fy = r.fscal * dy, fz = r.fscal * dz;
                                 fiacc[a - 32 * se.sci][0] += fx;
@@ -892,6 +954,8 @@ void ora_force(int n_sci, const nbx_sci_entry* sci, const nbx_cj_entry* cj,
     }
     if (e2) { e2[0] += elj; e2[1] += ec; }
     if (fshift) for (int k = 0; k < 3 * NBX_NSHIFT; k++) fshift[k] += fsh[k];
+    free(ftab);
+    free(vtab);
 }
 
 long long ora_count_pairs(int n_sci, const nbx_sci_entry* sci, const nbx_cj_entry* cj,

@@ -27,6 +27,8 @@ typedef struct ora_grid ora_grid;
 typedef struct ora_list ora_list;
 
 int ora_derive_consts(const nbx_params* p, nbx_consts* out);
+/* EWALD_TAB (value, next - value) tables, 2 * c->tab_n floats each (include/nbx.h). */
+int ora_ewald_table(const nbx_consts* c, float* ftab, float* vtab);
 
 /* Column grid dimensions: identical formula to the library. */
 void ora_grid_dims(const float size[3], double density, int* ncx, int* ncy, float inv_cell[2]);

@@ -40,7 +40,7 @@ class Consts(C.Structure):
     _fields_ = [(n, C.c_float) for n in ("epsfac", "k_rf", "c_rf", "beta", "sh_ewald", "sh_lj6",
                                          "sh_lj12", "rc2", "rlo2", "rli2", "fsw_r1", "fsw_a6", "fsw_b6",
                                          "fsw_a12", "fsw_b12", "fsw_p6", "fsw_q6", "fsw_p12", "fsw_q12",
-                                         "fsw_c6", "fsw_c12")]
+                                         "fsw_c6", "fsw_c12", "tab_scale")] + [("tab_n", C.c_int32)]
 
 
 class ListSizes(C.Structure):
@@ -62,6 +62,7 @@ def lib():
         L = C.CDLL(LIB)
         vp = C.c_void_p
         L.ora_derive_consts.argtypes = [C.POINTER(Params), C.POINTER(Consts)]
+        L.ora_ewald_table.argtypes = [C.POINTER(Consts), C.c_void_p, C.c_void_p]
         L.ora_grid_build.restype = vp
         L.ora_grid_build.argtypes = [C.c_int, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_double]
         L.ora_grid_free.argtypes = [vp]
@@ -100,8 +101,19 @@ def _p(a):
 
 def make_params(coulomb="ewald", rc=1.0, rlist_outer=1.1, rlist_inner=1.02, epsilon_r=1.0,
                 epsilon_rf=0.0, ewald_rtol=1e-5, lj_modifier="pot-shift", rvdw_switch=0.0) -> Params:
-    return Params(1 if coulomb == "ewald" else 0, rc, rlist_outer, rlist_inner, epsilon_r,
+    return Params({"rf": 0, "ewald": 1, "ewald-tab": 2}[coulomb], rc, rlist_outer, rlist_inner, epsilon_r,
                   epsilon_rf, ewald_rtol, {"pot-shift": 0, "force-switch": 1}[lj_modifier], rvdw_switch)
+
+
+def ewald_table(params: Params):
+    """EWALD_TAB (value, next - value) tables: (ftab[tab_n, 2], vtab[tab_n, 2])."""
+    c = Consts()
+    lib().ora_derive_consts(C.byref(params), C.byref(c))
+    ft = np.zeros((c.tab_n, 2), np.float32)
+    vt = np.zeros((c.tab_n, 2), np.float32)
+    if lib().ora_ewald_table(C.byref(c), _p(ft), _p(vt)):
+        raise ValueError("no Ewald table for these parameters")
+    return ft, vt
 
 
 def derive_consts(params: Params) -> dict:

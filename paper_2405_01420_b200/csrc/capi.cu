@@ -48,9 +48,14 @@ static int derive(const nbx_params* p, nbx_consts* c)
               ((2.0 * (double)p->epsilon_rf + (double)p->epsilon_r) * rc * rc * rc);
     c->k_rf = (float)krf;
     c->c_rf = (float)(1.0 / rc + krf * rc * rc);
-    const double beta = (p->coulomb_type == NBX_COULOMB_EWALD) ? ewald_beta(rc, p->ewald_rtol) : 0.0;
+    const bool ew = p->coulomb_type == NBX_COULOMB_EWALD || p->coulomb_type == NBX_COULOMB_EWALD_TAB;
+    const double beta = ew ? ewald_beta(rc, p->ewald_rtol) : 0.0;
     c->beta = (float)beta;
-    c->sh_ewald = (p->coulomb_type == NBX_COULOMB_EWALD) ? (float)(std::erfc(beta * rc) / rc) : 0.0f;
+    c->sh_ewald = ew ? (float)(std::erfc(beta * rc) / rc) : 0.0f;
+    if (p->coulomb_type == NBX_COULOMB_EWALD_TAB) {
+        c->tab_scale = (float)(400.0 * beta > 600.0 ? 400.0 * beta : 600.0);
+        c->tab_n = (int32_t)std::ceil(rc * (double)c->tab_scale) + 2;
+    }
     c->sh_lj6 = (float)(1.0 / (rc * rc * rc * rc * rc * rc));
     c->sh_lj12 = (float)(1.0 / (rc * rc * rc * rc * rc * rc * rc * rc * rc * rc * rc * rc));
     c->rc2 = (float)(rc * rc);
@@ -81,9 +86,41 @@ static int derive(const nbx_params* p, nbx_consts* c)
     if (p->lj_modifier != NBX_LJ_POT_SHIFT && p->lj_modifier != NBX_LJ_FORCE_SWITCH) return 1;
     if (p->lj_modifier == NBX_LJ_FORCE_SWITCH && !(p->rvdw_switch >= 0.0f && p->rvdw_switch < p->rc)) return 1;
     if (!(p->rc > 0.0f) || p->rlist_inner < p->rc || p->rlist_outer < p->rlist_inner) return 1;
-    if (p->coulomb_type != NBX_COULOMB_RF && p->coulomb_type != NBX_COULOMB_EWALD) return 1;
-    if (p->coulomb_type == NBX_COULOMB_EWALD && !(p->ewald_rtol > 0.0f && p->ewald_rtol < 1.0f)) return 1;
+    if (p->coulomb_type != NBX_COULOMB_RF && !ew) return 1;
+    if (ew && !(p->ewald_rtol > 0.0f && p->ewald_rtol < 1.0f)) return 1;
     if (!(p->epsilon_r > 0.0f)) return 1;
+    return 0;
+}
+
+// EWALD_TAB tables, identical formulas to ora_ewald_table (oracle/nbx_oracle.c): nodes
+// r_k = k / tab_scale; force correction beta^3 G(beta^2 r^2) with its series below z = 1e-2,
+// potential erf(beta r) / r; stored as (value, next - value)
+static double ewald_fcorr(double beta, double r)
+{
+    const double z = beta * beta * r * r, b3 = beta * beta * beta, tsp = 2.0 / std::sqrt(M_PI);
+    if (z < 1e-2) return tsp * b3 * (2.0 / 3.0 + z * (-2.0 / 5.0 + z * (1.0 / 7.0 + z * (-1.0 / 27.0 + z / 132.0))));
+    return (std::erf(beta * r) / r - tsp * beta * std::exp(-z)) / (r * r);
+}
+
+static double ewald_vcorr(double beta, double r)
+{
+    if (r == 0.0) return 2.0 * beta / std::sqrt(M_PI);
+    return std::erf(beta * r) / r;
+}
+
+int ewald_table(const nbx_consts* c, float* ftab, float* vtab)
+{
+    const int n = c->tab_n;
+    if (n < 2 || !(c->tab_scale > 0.0f)) return 1;
+    const double beta = c->beta, h = 1.0 / (double)c->tab_scale;
+    for (int k = 0; k < n; k++) {
+        ftab[2 * k] = (float)ewald_fcorr(beta, k * h);
+        vtab[2 * k] = (float)ewald_vcorr(beta, k * h);
+    }
+    for (int k = 0; k < n; k++) {
+        ftab[2 * k + 1] = (k + 1 < n) ? ftab[2 * k + 2] - ftab[2 * k] : 0.0f;
+        vtab[2 * k + 1] = (k + 1 < n) ? vtab[2 * k + 2] - vtab[2 * k] : 0.0f;
+    }
     return 0;
 }
 
@@ -126,6 +163,13 @@ NBX_API int nbx_derive_consts(const nbx_params* p, nbx_consts* out)
     return NBX_OK;
 }
 
+NBX_API int nbx_ewald_table(const nbx_consts* c, float* ftab, float* vtab)
+{
+    if (!c || !ftab || !vtab) return fail(NBX_EINVAL, "null argument");
+    if (ewald_table(c, ftab, vtab)) return fail(NBX_EINVAL, "constants carry no Ewald table (coulomb_type != EWALD_TAB)");
+    return NBX_OK;
+}
+
 NBX_API int nbx_create(int device, const nbx_params* p, nbx_ctx** out)
 {
     NBX_GUARD_BEGIN
@@ -150,6 +194,13 @@ NBX_API int nbx_create(int device, const nbx_params* p, nbx_ctx** out)
     ctx->c = c;
     ctx->acc.ensure(2 + 3 * NBX_NSHIFT + 9);
     NBX_CUDA(cudaMemset(ctx->acc.p, 0, sizeof(double) * (2 + 3 * NBX_NSHIFT + 9)));
+    if (p->coulomb_type == NBX_COULOMB_EWALD_TAB) {
+        std::vector<float> ft(2 * (size_t)c.tab_n), vt(2 * (size_t)c.tab_n);
+        ewald_table(&c, ft.data(), vt.data());
+        ctx->ewtab.ensure(2 * (size_t)c.tab_n); // [tab_n] force pairs, then [tab_n] potential pairs
+        NBX_CUDA(cudaMemcpy(ctx->ewtab.p, ft.data(), sizeof(float) * ft.size(), cudaMemcpyHostToDevice));
+        NBX_CUDA(cudaMemcpy(ctx->ewtab.p + c.tab_n, vt.data(), sizeof(float) * vt.size(), cudaMemcpyHostToDevice));
+    }
     ctx->sumq2.ensure(2);
     NBX_CUDA(cudaMemset(ctx->sumq2.p, 0, sizeof(double) * 2));
     ctx->counter.ensure(8);
@@ -184,6 +235,7 @@ NBX_API int nbx_destroy(nbx_ctx* ctx)
     }
     ctx->q_g.release(); ctx->type_g.release(); ctx->excl_off_g.release(); ctx->excl_gid_g.release();
     ctx->c6c12s.release(); ctx->acc.release(); ctx->sumq2.release(); ctx->counter.release();
+    ctx->ewtab.release();
     for (auto& g : ctx->graphs) cudaGraphExecDestroy(g.exec);
     peer_release(ctx);
     if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
@@ -503,7 +555,7 @@ NBX_API int nbx_energies(nbx_ctx* ctx, double* e, double* vir, void* stream)
     NBX_CUDA(cudaMemcpyAsync(&q2, ctx->sumq2.p, sizeof(double), cudaMemcpyDeviceToHost, st));
     NBX_CUDA(cudaStreamSynchronize(st));
     double self;
-    if (ctx->p.coulomb_type == NBX_COULOMB_EWALD)
+    if (ctx->p.coulomb_type == NBX_COULOMB_EWALD || ctx->p.coulomb_type == NBX_COULOMB_EWALD_TAB)
         self = -(double)ctx->c.epsfac * q2 * (double)ctx->c.beta / std::sqrt(M_PI);
     else
         self = -0.5 * (double)ctx->c.epsfac * (double)ctx->c.c_rf * q2;

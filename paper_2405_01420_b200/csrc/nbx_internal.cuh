@@ -96,6 +96,7 @@ struct Peer; // peer.cu: NVLink peer-memory halo state (DD, row e)
 struct ForceConsts {
     float epsfac, k_rf, two_k_rf, c_rf, beta, beta2, beta3, beta3_monic, sh_ewald, sh_lj6, sh_lj12, rc2, rli2;
     float fsw_r1, fsw_a6, fsw_b6, fsw_a12, fsw_b12, fsw_p6, fsw_q6, fsw_p12, fsw_q12, fsw_c6, fsw_c12;
+    float tab_scale;
 };
 
 } // namespace nbx
@@ -114,6 +115,7 @@ struct nbx_ctx {
     nbx::DBuf<int> type_g;
     nbx::DBuf<int> excl_off_g, excl_gid_g;
     nbx::DBuf<float2> c6c12s; // (6 c6, 12 c12)
+    nbx::DBuf<float2> ewtab;  // EWALD_TAB: [tab_n] (F, dF) then [tab_n] (V, dV)
     nbx::Grid grid[2];
     nbx::List list[2];
     nbx::DBuf<double> acc;    // [0..1] E_lj, E_coul ; [2..82] fshift ; [83..91] sum x (x) f

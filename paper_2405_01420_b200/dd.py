@@ -590,7 +590,9 @@ def bench(args, METRIC, UNIT, FLOPS_PER_PAIR, DESC, ClockSampler, time_cpu_port,
     clk = clocks.stop()
     step_ms = sorted(evs[k].elapsed_time(evs[k + 1]) for k in range(K))
     search_ms = [evs[k].elapsed_time(evs[k + 1]) for k in search_steps]
-    # per-phase breakdown on 10 extra (untimed) steps
+    # per-phase breakdown on 10 extra (untimed) steps, all ranks starting together
+    dist.barrier()
+    torch.cuda.synchronize()
     dd.profile_phases = True
     for k in range(10):
         dd.step(x_home, step=1)

@@ -21,7 +21,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("NBX_LIB") or os.path.join(HERE, "libnbx.so")  # NBX_LIB: variant builds (tools/)
 
-NBX_COULOMB_RF, NBX_COULOMB_EWALD = 0, 1
+NBX_COULOMB_RF, NBX_COULOMB_EWALD, NBX_COULOMB_EWALD_TAB = 0, 1, 2
 LIST_LOCAL, LIST_NONLOCAL = 0, 1
 FORCE_ENERGY, FORCE_VIRIAL = 1, 2
 
@@ -45,7 +45,7 @@ class Consts(C.Structure):
     _fields_ = [(n, C.c_float) for n in ("epsfac", "k_rf", "c_rf", "beta", "sh_ewald", "sh_lj6",
                                          "sh_lj12", "rc2", "rlo2", "rli2", "fsw_r1", "fsw_a6", "fsw_b6",
                                          "fsw_a12", "fsw_b12", "fsw_p6", "fsw_q6", "fsw_p12", "fsw_q12",
-                                         "fsw_c6", "fsw_c12")]
+                                         "fsw_c6", "fsw_c12", "tab_scale")] + [("tab_n", C.c_int32)]
 
 
 class ListSizes(C.Structure):
@@ -62,7 +62,7 @@ CJ_DTYPE = np.dtype([("cj", "<i4"), ("meta", "<u4")])
 POOL_DTYPE = np.dtype(("<u4", (8, 2)))
 
 # every symbol include/nbx.h declares (checked by tests/test_capi.py)
-EXPORTS = ["nbx_last_error", "nbx_version", "nbx_derive_consts", "nbx_create", "nbx_destroy",
+EXPORTS = ["nbx_last_error", "nbx_version", "nbx_derive_consts", "nbx_ewald_table", "nbx_create", "nbx_destroy",
            "nbx_set_topology", "nbx_set_box", "nbx_grid_build", "nbx_search", "nbx_put_x",
            "nbx_prune", "nbx_force", "nbx_get_f", "nbx_step_graph", "nbx_energies", "nbx_clear_energies",
            "nbx_grid_info_get", "nbx_grid_export", "nbx_list_sizes_get", "nbx_list_export",
@@ -85,6 +85,7 @@ def lib():
         L.nbx_last_error.restype = C.c_char_p
         L.nbx_version.restype = C.c_char_p
         L.nbx_derive_consts.argtypes = [C.POINTER(Params), C.POINTER(Consts)]
+        L.nbx_ewald_table.argtypes = [C.POINTER(Consts), vp, vp]
         L.nbx_create.argtypes = [C.c_int, C.POINTER(Params), C.POINTER(vp)]
         L.nbx_destroy.argtypes = [vp]
         L.nbx_set_topology.argtypes = [vp, i32, vp, vp, i32, vp, vp, vp]
@@ -130,7 +131,7 @@ LJ_MODIFIERS = {"pot-shift": 0, "force-switch": 1}
 
 def make_params(coulomb="ewald", rc=1.0, rlist_outer=1.1, rlist_inner=1.02, epsilon_r=1.0,
                 epsilon_rf=0.0, ewald_rtol=1e-5, lj_modifier="pot-shift", rvdw_switch=0.0) -> Params:
-    ct = {"rf": NBX_COULOMB_RF, "ewald": NBX_COULOMB_EWALD}[coulomb]
+    ct = {"rf": NBX_COULOMB_RF, "ewald": NBX_COULOMB_EWALD, "ewald-tab": NBX_COULOMB_EWALD_TAB}[coulomb]
     return Params(ct, rc, rlist_outer, rlist_inner, epsilon_r, epsilon_rf, ewald_rtol,
                   LJ_MODIFIERS[lj_modifier], rvdw_switch)
 

@@ -37,12 +37,41 @@ def test_exports_are_only_the_abi():
 @pytest.mark.parametrize("kw", [dict(coulomb="rf", rc=0.9, rlist_outer=1.0, rlist_inner=0.92),
                                 dict(coulomb="ewald", rc=1.0, rlist_outer=1.1, rlist_inner=1.02),
                                 dict(coulomb="ewald", rc=1.2, rlist_outer=1.3, rlist_inner=1.22, ewald_rtol=1e-6),
-                                dict(coulomb="rf", rc=1.0, rlist_outer=1.2, rlist_inner=1.05, epsilon_r=2.0, epsilon_rf=78.0)])
+                                dict(coulomb="rf", rc=1.0, rlist_outer=1.2, rlist_inner=1.05, epsilon_r=2.0, epsilon_rf=78.0),
+                                dict(coulomb="ewald-tab", rc=1.2, rlist_outer=1.3, rlist_inner=1.22,
+                                     lj_modifier="force-switch", rvdw_switch=1.0),
+                                dict(coulomb="ewald-tab", rc=0.9, rlist_outer=1.0, rlist_inner=0.92, ewald_rtol=1e-3)])
 def test_derived_constants_bit_identical(kw):
     a = nbx.derive_consts(nbx.make_params(**kw))
     b = O.derive_consts(O.make_params(**kw))
     for k in a:
         assert np.float32(a[k]).tobytes() == np.float32(b[k]).tobytes(), k
+
+
+@pytest.mark.parametrize("rc, rtol", [(1.2, 1e-5), (1.0, 1e-5), (0.9, 1e-3)])
+def test_ewald_tables_bit_identical(rc, rtol):
+    """EWALD_TAB tables: library (host side, no GPU needed) == oracle, and accurate."""
+    import ctypes as C
+    from scipy.special import erf
+    kw = dict(coulomb="ewald-tab", rc=rc, rlist_outer=rc + 0.1, rlist_inner=rc + 0.02, ewald_rtol=rtol)
+    c = nbx.Consts()
+    nbx.check(nbx.lib().nbx_derive_consts(C.byref(nbx.make_params(**kw)), C.byref(c)))
+    assert c.tab_scale >= 600.0 and c.tab_n == int(np.ceil(rc * np.float64(c.tab_scale))) + 2
+    ft = np.zeros((c.tab_n, 2), np.float32)
+    vt = np.zeros((c.tab_n, 2), np.float32)
+    nbx.check(nbx.lib().nbx_ewald_table(C.byref(c), nbx._ptr(ft), nbx._ptr(vt)))
+    fo, vo = O.ewald_table(O.make_params(**kw))
+    assert ft.tobytes() == fo.tobytes() and vt.tobytes() == vo.tobytes()
+    # interpolation error at mid-points against the exact correction terms
+    b = np.float64(c.beta)
+    r = (np.arange(1, c.tab_n - 2) + 0.5) / np.float64(c.tab_scale)
+    fex = (erf(b * r) / r - 2 * b / np.sqrt(np.pi) * np.exp(-b * b * r * r)) / (r * r)
+    vex = erf(b * r) / r
+    k = np.arange(1, c.tab_n - 2)
+    fin = ft[k, 0] + 0.5 * ft[k, 1]
+    vin = vt[k, 0] + 0.5 * vt[k, 1]
+    assert np.abs(fin - fex).max() / fex.max() < 2e-6
+    assert np.abs(vin - vex).max() / vex.max() < 2e-6
 
 
 def test_invalid_params_rejected():

@@ -336,10 +336,12 @@ def test_graph_steps_match_eager(gpu):
 
 
 @pytest.mark.parametrize("natoms", [60000, None])
-def test_force_switch_flavour(gpu, natoms):
-    """Row f3: force-switch LJ kernels (F and VF) vs the oracle; None = full STMV size."""
+@pytest.mark.parametrize("config", ["stmv_fsw", "stmv_tab"])
+def test_force_switch_flavour(gpu, natoms, config):
+    """Row f3: force-switch LJ kernels (F and VF) vs the oracle, with the analytical or the
+    tabulated Ewald correction (stmv_tab: the paper's STMV kernel flavour); None = full STMV."""
     import torch
-    s = get_system("stmv_fsw", natoms)
+    s = get_system(config, natoms)
     nb, on, xd = run_pair(s)
     f, (e, vir) = nb.forces(xd, energy=True, virial=True)
     f2 = nb.forces(xd)

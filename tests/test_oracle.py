@@ -209,3 +209,26 @@ def test_force_switch_vs_brute_force():
     # the switched force vanishes continuously at rc: a pair just inside rc has ~0 LJ force
     cf = O.derive_consts(O.make_params(**s.params()))
     assert cf["fsw_r1"] == np.float32(1.0)
+
+
+def test_tabulated_ewald_vs_brute_force():
+    """Row f3: tabulated Ewald real space (the paper's kernel flavour) against float64 with
+    exact erfc, with force-switch LJ (the paper's STMV flavour)."""
+    s = systems.make("stmv_tab", 6000)
+    on = O.OracleNonbonded(s)
+    on.search(s.x)
+    f, e, vir, _ = on.forces()
+    c = O.derive_consts(on.params)
+    assert c["tab_n"] > 0
+    fb, eb, vb = brute_force(s.x, s.q, s.type, s.c6c12, s.excl_offsets, s.excl_gids, s.box, c, "ewald", s.rc,
+                             lj_modifier="force-switch", rvdw_switch=s.rvdw_switch)
+    assert np.sqrt(((f - fb) ** 2).sum() / (fb**2).sum()) < 5e-6
+    assert abs(e[0] - eb[0]) / abs(eb[0]) < 1e-5
+    assert abs(e[1] - eb[1]) / abs(eb[1]) < 1e-5
+    assert np.abs(vir - vb).max() / np.abs(vb).max() < 5e-6
+    # and close to the analytical-rational flavour on the same list
+    s2 = systems.make("stmv_fsw", 6000)
+    on2 = O.OracleNonbonded(s2)
+    on2.search(s2.x)
+    f2, e2, _, _ = on2.forces()
+    assert np.sqrt(((f - f2) ** 2).sum() / (f2**2).sum()) < 5e-6
