@@ -97,6 +97,8 @@ struct ForceConsts {
     float epsfac, k_rf, two_k_rf, c_rf, beta, beta2, beta3, beta3_monic, sh_ewald, sh_lj6, sh_lj12, rc2, rli2;
     float fsw_r1, fsw_a6, fsw_b6, fsw_a12, fsw_b12, fsw_p6, fsw_q6, fsw_p12, fsw_q12, fsw_c6, fsw_c12;
     float tab_scale;
+    float rc2_big;   // rc2 * 2^64: cut-off step as one FFMA.SAT (force-only kernels)
+    unsigned one;    // 1, opaque to the compiler: integer adds issued as IMAD (FMA pipe)
 };
 
 } // namespace nbx
@@ -154,6 +156,14 @@ __device__ __forceinline__ void red_add_v4(float4* p, float4 v)
 {
     asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y),
                  "f"(v.z), "f"(v.w)
+                 : "memory");
+}
+
+// predicated v4 reduction (no branch / reconvergence around the lanes that write)
+__device__ __forceinline__ void red_add_v4_if(float4* p, float4 v, unsigned cond)
+{
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %5, 0;\n\t@q red.global.add.v4.f32 [%0], {%1,%2,%3,%4};\n\t}"
+                 ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(cond)
                  : "memory");
 }
 

@@ -12,9 +12,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "scratch", "variants")
 VARIANTS = {
     "base": [],
-    "xismem_b2": ["-DNBX_XI_SMEM=1"],
-    "xismem_b3": ["-DNBX_XI_SMEM=1", "-DNBX_FORCE_MINB=3"],
-    "xismem_t128b6": ["-DNBX_XI_SMEM=1", "-DNBX_FORCE_THREADS=128", "-DNBX_FORCE_MINB=6"],
+    "jred16u2": ["-DNBX_JRED16=1", "-DNBX_EUNROLL=2"],
+    "jred32u2": ["-DNBX_JRED16=2", "-DNBX_EUNROLL=2"],
+    "jred16u4": ["-DNBX_JRED16=1", "-DNBX_EUNROLL=4"],
 }
 
 
@@ -55,10 +55,21 @@ def run_one(name, cfg, reps=20):
     e1.record(st)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
-    nb.get_f(f)
+    f.zero_()
+    nb.forces(x, out=f)
+    torch.cuda.synchronize()
     p, sl = nb.count_pairs()
-    return {"variant": name, "config": cfg, "force_ms": ms, "slot_tflops": sl * 57 / ms / 1e9,
-            "pairs_per_s": p / ms * 1e3}
+    tag = name + ("_packed" if os.environ.get("NBX_PACKED_FORCE") == "1" else "")
+    import numpy as np
+    fn = f.cpu().numpy().astype(np.float64)
+    np.save(os.path.join(OUT, f"f_{tag}_{cfg}.npy"), fn)
+    out = {"variant": tag, "config": cfg, "force_ms": ms, "slot_tflops": sl * 57 / ms / 1e9,
+           "pairs_per_s": p / ms * 1e3}
+    ref = os.path.join(OUT, f"f_base_{cfg}.npy")
+    if os.path.exists(ref) and tag != "base":
+        fr = np.load(ref)
+        out["rel_rms_vs_base"] = float(np.sqrt(((fn - fr) ** 2).sum() / (fr ** 2).sum()))
+    return out
 
 
 if __name__ == "__main__":
