@@ -12,9 +12,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "scratch", "variants")
 VARIANTS = {
     "base": [],
-    "jred16u2": ["-DNBX_JRED16=1", "-DNBX_EUNROLL=2"],
-    "jred32u2": ["-DNBX_JRED16=2", "-DNBX_EUNROLL=2"],
-    "jred16u4": ["-DNBX_JRED16=1", "-DNBX_EUNROLL=4"],
+    "ewz": ["-DNBX_EWR2=0"],
+    "qreg": ["-DNBX_QREG=1"],
 }
 
 
