@@ -751,11 +751,11 @@ static inline pairres pair_eval(float dx, float dy, float dz, int masked, int in
     if (masked) r2 = fmaxf(r2, R2MIN);
     float rinv = 1.0f / sqrtf(r2);
     float rinv2 = rinv * rinv;
-    float rinv6 = (rinv2 * rinv2) * rinv2;
+    float rinv3 = rinv * rinv2;
+    float rinv6 = rinv3 * rinv3;
     float fint = masked ? (float)intb : 1.0f;
     float flj = (rinv6 * fmaf(c12, rinv6, -c6)) * fint;
     float qq = qi * qj;
-    float rinv3 = rinv * rinv2;
     float fc, z = 0.0f;
     if (coul == NBX_COULOMB_RF) {
         fc = qq * fmaf(fint, rinv3, -(c->k_rf * 2.0f));

@@ -12,8 +12,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "scratch", "variants")
 VARIANTS = {
     "base": [],
-    "ewz": ["-DNBX_EWR2=0"],
-    "qreg": ["-DNBX_QREG=1"],
+    "ri6": ["-DNBX_RI6=1"],
+    "pred": ["-DNBX_PREDACC=1"],
+    "ewn5": ["-DNBX_EWN5=1"],
+    "all3": ["-DNBX_RI6=1", "-DNBX_PREDACC=1", "-DNBX_EWN5=1"],
 }
 
 
