@@ -32,6 +32,8 @@ UNIT = "pair-interactions/s"
 # Algorithmic FP32 flops per in-cut-off pair of the force-only kernel, counted once from
 # pairmath.cuh / force.cu (FADD/FMUL/MUFU = 1, FFMA = 2) and frozen.
 FLOPS_PER_PAIR = {"ewald": 57, "rf": 33, "ewald-tab": 43}
+# combination-rule LJ adds the per-pair parameter arithmetic (nbx.h NBX_LJ_COMB_*)
+LJ_EXTRA_FLOPS = {"comb-geom": 2, "comb-lb": 8}
 DESC = {
     "water3k": "SPC/E water box 3k atoms (1k waters), reaction-field, rc=0.9 nm",
     "rnase24k": "RNase-sized 24,024-atom solvated protein-like box, Ewald real-space, rc=1.0 nm",
@@ -40,11 +42,14 @@ DESC = {
     "stmv_fsw": "STMV-sized box with force-switch LJ (rvdw_switch 1.0 nm, rc 1.2 nm), Ewald",
     "stmv_tab": "STMV-sized box, the paper's STMV kernel flavour: tabulated Ewald + force-switch LJ, rc 1.2 nm",
     "water12m": "12M-atom water box, Ewald, rc=1.0 nm (strong-scaling sweep 1/2/4/8)",
+    "rnase24k_lb": "RNase-sized 24,024-atom protein-like box, Ewald, Lorentz-Berthelot combination-rule LJ",
+    "rnase24k_geom": "RNase-sized 24,024-atom protein-like box, Ewald, geometric combination-rule LJ",
+    "grappa1.5m": "Grappa kernel flavour (tabulated Ewald + LB combination-rule LJ), 1.5M-atom uniform water box, rc=1.0 nm",
 }
 L2_BYTES = 126 * 1024 * 1024
 NATOMS = {"water3k": 3000, "rnase24k": 24024, "mem82k": 82000, "stmv": 1066628, "stmv_fsw": 1066628,
           "stmv_tab": 1066628,
-          "water12m": 12_000_000}
+          "water12m": 12_000_000, "rnase24k_lb": 24024, "rnase24k_geom": 24024, "grappa1.5m": 1_500_000}
 
 
 def parse():
@@ -258,7 +263,7 @@ def run_single(args):
     ms_per_step = tot_ms / K
     value = pairs * K / (tot_ms * 1e-3)
     t_force = sum(force_ms) / K
-    fl = FLOPS_PER_PAIR[s.coulomb]
+    fl = FLOPS_PER_PAIR[s.coulomb] + LJ_EXTRA_FLOPS.get(s.lj_modifier, 0)
     achieved = pairs * fl / (t_force * 1e-3) / 1e12
     slot_tf = slots * fl / (t_force * 1e-3) / 1e12
 

@@ -48,8 +48,18 @@ typedef enum {
  * the paper's kernel flavour for both its benchmarks. */
 enum { NBX_COULOMB_RF = 0, NBX_COULOMB_EWALD = 1, NBX_COULOMB_EWALD_TAB = 2 };
 /* LJ modifiers: potential shift (default) or force switch between rvdw_switch and rc
- * (the CHARMM/STMV flavour of the paper) */
-enum { NBX_LJ_POT_SHIFT = 0, NBX_LJ_FORCE_SWITCH = 1 };
+ * (the CHARMM/STMV flavour of the paper).
+ * COMB_GEOM / COMB_LB: potential-shifted LJ with a combination rule -- the "Lennard-Jones
+ * with combination rule" kernel flavour of the paper's Grappa benchmarks.
+ * Pair parameters come from per-type parameters derived (in double, rounded once) from the
+ * table's diagonal instead of from the type-pair table:
+ *   GEOM: p_t = (sqrt(6 c6_tt), sqrt(12 c12_tt));   6 c6_ij = p6_i p6_j, 12 c12_ij = p12_i p12_j
+ *   LB:   sigma_t^6 = c12_tt / c6_tt, eps_t = c6_tt^2 / (4 c12_tt) (0, 0 for c6_tt = 0);
+ *         p_t = (sigma_t / 2, sqrt(24 eps_t));  s = s_i + s_j, s6 = ((s s)(s s))(s s),
+ *         6 c6_ij = (e_i e_j) s6, 12 c12_ij = 2 ((6 c6_ij) s6)
+ * nbx_set_topology checks that every off-diagonal table entry follows the rule (relative
+ * 1e-4) and fails with NBX_EINVAL otherwise.                                              */
+enum { NBX_LJ_POT_SHIFT = 0, NBX_LJ_FORCE_SWITCH = 1, NBX_LJ_COMB_GEOM = 2, NBX_LJ_COMB_LB = 3 };
 
 typedef struct nbx_params {
     int32_t coulomb_type; /* NBX_COULOMB_RF, NBX_COULOMB_EWALD or NBX_COULOMB_EWALD_TAB     */
@@ -59,7 +69,7 @@ typedef struct nbx_params {
     float epsilon_r;      /* relative dielectric constant                                  */
     float epsilon_rf;     /* reaction-field dielectric; 0 means infinity                   */
     float ewald_rtol;     /* erfc(beta*rc) = ewald_rtol                                    */
-    int32_t lj_modifier;  /* NBX_LJ_POT_SHIFT or NBX_LJ_FORCE_SWITCH                         */
+    int32_t lj_modifier;  /* NBX_LJ_POT_SHIFT, NBX_LJ_FORCE_SWITCH, NBX_LJ_COMB_GEOM, _LB     */
     float rvdw_switch;    /* force-switch start r1, 0 <= r1 < rc (ignored for POT_SHIFT)   */
 } nbx_params;
 

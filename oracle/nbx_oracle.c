@@ -799,6 +799,44 @@ static inline pairres pair_eval(float dx, float dy, float dz, int masked, int in
     return r;
 }
 
+/* LJ combination rules (nbx.h NBX_LJ_COMB_*): per-type parameters from the table diagonal,
+ * in double, rounded once; zero for other modifiers.  Rule violations are not checked here
+ * (the library's nbx_set_topology rejects them). */
+void ora_lj_comb_params(int ljmod, int ntypes, const float* c6c12, float* pt)
+{
+    for (int a = 0; a < ntypes; a++) {
+        const double c6 = c6c12[2 * (a * ntypes + a)], c12 = c6c12[2 * (a * ntypes + a) + 1];
+        pt[2 * a] = pt[2 * a + 1] = 0.0f;
+        if (ljmod == NBX_LJ_COMB_GEOM) {
+            pt[2 * a] = (float)sqrt(6.0 * c6);
+            pt[2 * a + 1] = (float)sqrt(12.0 * c12);
+        } else if (ljmod == NBX_LJ_COMB_LB && c6 > 0.0 && c12 > 0.0) {
+            const double sig = sqrt(cbrt(c12 / c6)), eps = c6 * c6 / (4.0 * c12);
+            pt[2 * a] = (float)(0.5 * sig);
+            pt[2 * a + 1] = (float)sqrt(24.0 * eps);
+        }
+    }
+}
+
+/* (6 c6, 12 c12) of a type pair: table lookup, or the combination rule in fp32 */
+static inline void lj_pair(int ljmod, const float* pt, const float* c6c12, int ntypes, int ti, int tj,
+                           float* c6, float* c12)
+{
+    if (ljmod == NBX_LJ_COMB_GEOM) {
+        *c6 = pt[2 * ti] * pt[2 * tj];
+        *c12 = pt[2 * ti + 1] * pt[2 * tj + 1];
+    } else if (ljmod == NBX_LJ_COMB_LB) {
+        const float sg = pt[2 * ti] + pt[2 * tj], s2 = sg * sg, s6 = (s2 * s2) * s2;
+        const float p6 = (pt[2 * ti + 1] * pt[2 * tj + 1]) * s6;
+        *c6 = p6;
+        *c12 = 2.0f * (p6 * s6);
+    } else {
+        const float* cc = c6c12 + 2 * (ti * ntypes + tj);
+        *c6 = 6.0f * cc[0];
+        *c12 = 12.0f * cc[1];
+    }
+}
+
 void ora_force(int n_sci, const nbx_sci_entry* sci, const nbx_cj_entry* cj,
                const nbx_mask_pool_entry* pool, const float* xq_i, const int* type_i,
                const float* xq_j, const int* type_j, int ntypes, const float* c6c12,
@@ -808,6 +846,8 @@ void ora_force(int n_sci, const nbx_sci_entry* sci, const nbx_cj_entry* cj,
     nbx_consts c;
     ora_derive_consts(p, &c);
     const int coul = p->coulomb_type, energy = (flags & NBX_FORCE_ENERGY) != 0, ljmod = p->lj_modifier;
+    float* ptype = (float*)malloc(sizeof(float) * 2 * (size_t)ntypes);
+    ora_lj_comb_params(ljmod, ntypes, c6c12, ptype);
     float* ftab = NULL;
     float* vtab = NULL;
     if (coul == NBX_COULOMB_EWALD_TAB) {
@@ -852,8 +892,8 @@ void ora_force(int n_sci, const nbx_sci_entry* sci, const nbx_cj_entry* cj,
                             const float* xb = xq_j + 4 * b;
                             float dx = xs - xb[0], dy = ys - xb[1], dz = zs - xb[2];
                             int bit = i * 8 + j;
-                            const float* cc = c6c12 + 2 * (ti * ntypes + type_j[b]);
-                            float c6 = 6.0f * cc[0], c12 = 12.0f * cc[1];
+                            float c6, c12;
+                            lj_pair(ljmod, ptype, c6c12, ntypes, ti, type_j[b], &c6, &c12);
                             pairres r = pair_eval(dx, dy, dz, masked, (im >> bit) & 1, (cm >> bit) & 1,
                                                   qi, xb[3], c6, c12, &c, coul, energy, ljmod, ftab, vtab);
                             if (!r.valid) continue;
@@ -918,8 +958,8 @@ void ora_force(int n_sci, const nbx_sci_entry* sci, const nbx_cj_entry* cj,
                                 const float* xb = xq_j + 4 * b;
                                 float dx = xs - xb[0], dy = ys - xb[1], dz = zs - xb[2];
                                 int bit = i * 8 + j;
-                                const float* cc = c6c12 + 2 * (ti * ntypes + type_j[b]);
-                                float c6 = 6.0f * cc[0], c12 = 12.0f * cc[1];
+                                float c6, c12;
+                                lj_pair(ljmod, ptype, c6c12, ntypes, ti, type_j[b], &c6, &c12);
                                 pairres r = pair_eval(dx, dy, dz, masked, (im >> bit) & 1, (cm >> bit) & 1,
                                                       qi, xb[3], c6, c12, &c, coul, energy, ljmod, ftab, vtab);
                                 if (!r.valid) continue;
@@ -954,6 +994,7 @@ void ora_force(int n_sci, const nbx_sci_entry* sci, const nbx_cj_entry* cj,
     }
     if (e2) { e2[0] += elj; e2[1] += ec; }
     if (fshift) for (int k = 0; k < 3 * NBX_NSHIFT; k++) fshift[k] += fsh[k];
+    free(ptype);
     free(ftab);
     free(vtab);
 }

@@ -64,6 +64,9 @@ void ora_prune(ora_list* l, const ora_grid* gi, const ora_grid* gj, const nbx_pa
  * c6c12 is the plain (c6, c12) table [ntypes*ntypes*2].  f_i/f_j are double [nslots*3]
  * accumulators (may alias when gi == gj); e2 = {E_lj, E_coul} (no self term);
  * fshift = double[27*3].  energy/shift flags as NBX_FORCE_*. nthreads <= 0 = all.       */
+/* per-type LJ parameters of the combination rules (pt: 2 * ntypes floats) */
+void ora_lj_comb_params(int ljmod, int ntypes, const float* c6c12, float* pt);
+
 void ora_force(int n_sci, const nbx_sci_entry* sci, const nbx_cj_entry* cj,
                const nbx_mask_pool_entry* pool, const float* xq_i, const int* type_i,
                const float* xq_j, const int* type_j, int ntypes, const float* c6c12,

@@ -63,6 +63,7 @@ def lib():
         vp = C.c_void_p
         L.ora_derive_consts.argtypes = [C.POINTER(Params), C.POINTER(Consts)]
         L.ora_ewald_table.argtypes = [C.POINTER(Consts), C.c_void_p, C.c_void_p]
+        L.ora_lj_comb_params.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_float), C.POINTER(C.c_float)]
         L.ora_grid_build.restype = vp
         L.ora_grid_build.argtypes = [C.c_int, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_double]
         L.ora_grid_free.argtypes = [vp]
@@ -102,7 +103,7 @@ def _p(a):
 def make_params(coulomb="ewald", rc=1.0, rlist_outer=1.1, rlist_inner=1.02, epsilon_r=1.0,
                 epsilon_rf=0.0, ewald_rtol=1e-5, lj_modifier="pot-shift", rvdw_switch=0.0) -> Params:
     return Params({"rf": 0, "ewald": 1, "ewald-tab": 2}[coulomb], rc, rlist_outer, rlist_inner, epsilon_r,
-                  epsilon_rf, ewald_rtol, {"pot-shift": 0, "force-switch": 1}[lj_modifier], rvdw_switch)
+                  epsilon_rf, ewald_rtol, {"pot-shift": 0, "force-switch": 1, "comb-geom": 2, "comb-lb": 3}[lj_modifier], rvdw_switch)
 
 
 def ewald_table(params: Params):

@@ -83,7 +83,7 @@ static int derive(const nbx_params* p, nbx_consts* c)
         c->fsw_c6 = (float)C[0];
         c->fsw_c12 = (float)C[1];
     }
-    if (p->lj_modifier != NBX_LJ_POT_SHIFT && p->lj_modifier != NBX_LJ_FORCE_SWITCH) return 1;
+    if (p->lj_modifier < NBX_LJ_POT_SHIFT || p->lj_modifier > NBX_LJ_COMB_LB) return 1;
     if (p->lj_modifier == NBX_LJ_FORCE_SWITCH && !(p->rvdw_switch >= 0.0f && p->rvdw_switch < p->rc)) return 1;
     if (!(p->rc > 0.0f) || p->rlist_inner < p->rc || p->rlist_outer < p->rlist_inner) return 1;
     if (p->coulomb_type != NBX_COULOMB_RF && !ew) return 1;
@@ -274,8 +274,43 @@ NBX_API int nbx_set_topology(nbx_ctx* ctx, int32_t n, const float* q, const int3
     if (nexcl > 0)
         NBX_CUDA(cudaMemcpy(ctx->excl_gid_g.p, excl_gids, sizeof(int) * nexcl, cudaMemcpyHostToDevice));
     std::vector<float2> t((size_t)ntypes * ntypes);
-    for (int k = 0; k < ntypes * ntypes; k++)
-        t[k] = make_float2(6.0f * c6c12[2 * k], 12.0f * c6c12[2 * k + 1]);
+    const int lj = ctx->p.lj_modifier;
+    if (lj == NBX_LJ_COMB_GEOM || lj == NBX_LJ_COMB_LB) {
+        // combination rule: per-type parameters (nbx.h) replace the type-pair table
+        t.resize(ntypes);
+        for (int a = 0; a < ntypes; a++) {
+            const double c6 = c6c12[2 * (a * ntypes + a)], c12 = c6c12[2 * (a * ntypes + a) + 1];
+            if (c6 < 0.0 || c12 < 0.0) return fail(NBX_EINVAL, "negative LJ parameters");
+            if (lj == NBX_LJ_COMB_GEOM) {
+                t[a] = make_float2((float)std::sqrt(6.0 * c6), (float)std::sqrt(12.0 * c12));
+            } else if (c6 > 0.0 && c12 > 0.0) {
+                const double sig = std::sqrt(std::cbrt(c12 / c6)), eps = c6 * c6 / (4.0 * c12);
+                t[a] = make_float2((float)(0.5 * sig), (float)std::sqrt(24.0 * eps));
+            } else {
+                if (c6 != 0.0 || c12 != 0.0)
+                    return fail(NBX_EINVAL, "Lorentz-Berthelot needs c6 and c12 both zero or both positive");
+                t[a] = make_float2(0.0f, 0.0f);
+            }
+        }
+        for (int a = 0; a < ntypes; a++)
+            for (int b = 0; b < ntypes; b++) {
+                float p6, p12;
+                if (lj == NBX_LJ_COMB_GEOM) {
+                    p6 = t[a].x * t[b].x;
+                    p12 = t[a].y * t[b].y;
+                } else {
+                    const float sg = t[a].x + t[b].x, s2 = sg * sg, s6 = (s2 * s2) * s2;
+                    p6 = (t[a].y * t[b].y) * s6;
+                    p12 = 2.0f * (p6 * s6);
+                }
+                const double w6 = 6.0 * c6c12[2 * (a * ntypes + b)], w12 = 12.0 * c6c12[2 * (a * ntypes + b) + 1];
+                if (std::fabs(p6 - w6) > 1e-4 * std::fabs(w6) + 1e-30 || std::fabs(p12 - w12) > 1e-4 * std::fabs(w12) + 1e-30)
+                    return fail(NBX_EINVAL, "LJ table does not follow the selected combination rule");
+            }
+    } else {
+        for (int k = 0; k < ntypes * ntypes; k++)
+            t[k] = make_float2(6.0f * c6c12[2 * k], 12.0f * c6c12[2 * k + 1]);
+    }
     ctx->c6c12s.ensure(t.size());
     NBX_CUDA(cudaMemcpy(ctx->c6c12s.p, t.data(), sizeof(float2) * t.size(), cudaMemcpyHostToDevice));
     ctx->have_topology = true;

@@ -629,7 +629,7 @@ def bench(args, METRIC, UNIT, FLOPS_PER_PAIR, DESC, ClockSampler, time_cpu_port,
     if rank == 0:
         ms_per_step = ms_max / K
         value = pairs_tot * K / (ms_max * 1e-3)
-        fl = FLOPS_PER_PAIR[s.coulomb]
+        fl = FLOPS_PER_PAIR[s.coulomb] + {"comb-geom": 2, "comb-lb": 8}.get(s.lj_modifier, 0)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,

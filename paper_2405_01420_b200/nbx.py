@@ -126,7 +126,7 @@ def check(code):
         raise NbxError(code, lib().nbx_last_error().decode())
 
 
-LJ_MODIFIERS = {"pot-shift": 0, "force-switch": 1}
+LJ_MODIFIERS = {"pot-shift": 0, "force-switch": 1, "comb-geom": 2, "comb-lb": 3}
 
 
 def make_params(coulomb="ewald", rc=1.0, rlist_outer=1.1, rlist_inner=1.02, epsilon_r=1.0,

@@ -302,7 +302,18 @@ CONFIGS = {
     "stmv_fsw": dict(desc="STMV box with force-switch LJ (rvdw_switch 1.0 nm, rc 1.2 nm)"),
     "stmv_tab": dict(desc="STMV box, the paper's STMV kernel flavour: tabulated Ewald + force-switch LJ"),
     "water12m": dict(desc="12M-atom water box, Ewald, rc=1.0 nm"),
+    "rnase24k_lb": dict(desc="RNase-sized protein-like box, Ewald, Lorentz-Berthelot combination-rule LJ"),
+    "rnase24k_geom": dict(desc="RNase-sized protein-like box (geometric LJ table), Ewald, geometric combination-rule LJ"),
+    "grappa1.5m": dict(desc="Grappa-flavour kernel (PAPER.md:235): tabulated Ewald + Lorentz-Berthelot combination-rule LJ, "
+                            "uniform-density 1.5M-atom water box, rc=1.0 nm"),
 }
+
+
+def geometric_table(c6c12: np.ndarray) -> np.ndarray:
+    """(c6, c12) table with geometric mixing of its diagonal: c_ij = sqrt(c_ii c_jj)."""
+    d = np.diagonal(c6c12.astype(np.float64), axis1=0, axis2=1).T  # [T, 2]
+    t = np.sqrt(d[:, None, :] * d[None, :, :])
+    return t.astype(np.float32)
 
 
 def make(name: str, natoms: int | None = None) -> System:
@@ -331,4 +342,19 @@ def make(name: str, natoms: int | None = None) -> System:
     if name == "water12m":
         n = natoms or 12_000_000
         return water_box(n // 3, seed=5, coulomb="ewald", rc=1.0, name="water12m")
+    if name == "rnase24k_lb":
+        # the generator's table is Lorentz-Berthelot mixed (_lj_table): the LB rule reproduces it
+        s = protein_box(natoms or 24024, seed=2, rc=1.0, name="rnase24k_lb")
+        s.lj_modifier = "comb-lb"
+        return s
+    if name == "rnase24k_geom":
+        s = protein_box(natoms or 24024, seed=2, rc=1.0, name="rnase24k_geom")
+        s.c6c12 = geometric_table(s.c6c12)
+        s.lj_modifier = "comb-geom"
+        return s
+    if name == "grappa1.5m":
+        n = natoms or 1_500_000
+        s = water_box(n // 3, seed=6, coulomb="ewald", rc=1.0, name="grappa1.5m")
+        s.coulomb, s.lj_modifier = "ewald-tab", "comb-lb"
+        return s
     raise KeyError(f"unknown system {name!r}; known: {sorted(CONFIGS)}")

@@ -351,3 +351,35 @@ def test_force_switch_flavour(gpu, natoms, config):
     assert_forces(f2.cpu().numpy(), fo)
     assert_energies(e, eo)
     assert_virial(vir, viro)
+
+
+@pytest.mark.parametrize("config,natoms", [("rnase24k_lb", None), ("rnase24k_geom", None), ("grappa1.5m", 60000),
+                                           ("grappa1.5m", None)])
+def test_combination_rule_flavour(gpu, config, natoms):
+    """Row f3: combination-rule LJ kernels (F and VF; grappa1.5m = the paper's Grappa flavour,
+    tabulated Ewald + LB rule, at full size) vs the oracle: lists bit-exact, forces, energies
+    and virial within the north_star tolerances."""
+    import torch
+    s = get_system(config, natoms)
+    nb, on, xd = run_pair(s)
+    assert_lists_equal(nb.pairlist(1), on.list.export(1), config)
+    f, (e, vir) = nb.forces(xd, energy=True, virial=True)
+    f2 = nb.forces(xd)
+    torch.cuda.synchronize()
+    fo, eo, viro, _ = on.forces()
+    assert_forces(f.cpu().numpy(), fo)
+    assert_forces(f2.cpu().numpy(), fo)
+    assert_energies(e, eo)
+    assert_virial(vir, viro)
+
+
+def test_combination_rule_table_check(gpu):
+    """A table that does not follow the selected rule is rejected (NBX_EINVAL), not silently
+    replaced: the generator's LB-mixed protein table is not geometric."""
+    from paper_2405_01420_b200 import nbx
+    s = systems.make("rnase24k", 3000)
+    s.lj_modifier = "comb-geom"
+    with pytest.raises(nbx.NbxError, match="combination rule"):
+        nbx.Nonbonded(s, device=0)
+    s.lj_modifier = "comb-lb"
+    nbx.Nonbonded(s, device=0)  # LB-mixed: accepted

@@ -232,3 +232,48 @@ def test_tabulated_ewald_vs_brute_force():
     on2.search(s2.x)
     f2, e2, _, _ = on2.forces()
     assert np.sqrt(((f - f2) ** 2).sum() / (f2**2).sum()) < 5e-6
+
+
+@pytest.mark.parametrize("config", ["rnase24k_lb", "rnase24k_geom"])
+def test_combination_rule_vs_brute_force(config):
+    """Row f3: combination-rule LJ (the paper's Grappa kernel flavour).  The
+    oracle's per-pair parameters come from per-type parameters, the brute force uses the
+    (LB- or geometric-mixed) float64 table: forces, energies and virial agree."""
+    s = systems.make(config, 3000)
+    on = O.OracleNonbonded(s)
+    on.search(s.x)
+    f, e, vir, _ = on.forces()
+    c = O.derive_consts(on.params)
+    fb, eb, vb = brute_force(s.x, s.q, s.type, s.c6c12, s.excl_offsets, s.excl_gids, s.box, c, s.coulomb, s.rc)
+    assert np.sqrt(((f - fb) ** 2).sum() / (fb**2).sum()) < 5e-6
+    assert abs(e[0] - eb[0]) / abs(eb[0]) < 1e-5
+    assert np.abs(vir - vb).max() / np.abs(vb).max() < 5e-6
+    # the per-pair parameters reproduce the table (float rounding only)
+    import ctypes as C
+    nt = s.c6c12.shape[0]
+    pt = np.zeros(2 * nt, dtype=np.float32)
+    tab = np.ascontiguousarray(s.c6c12, dtype=np.float32)
+    mod = {"comb-geom": 2, "comb-lb": 3}[s.lj_modifier]
+    O.lib().ora_lj_comb_params(mod, nt, tab.ctypes.data_as(C.POINTER(C.c_float)), pt.ctypes.data_as(C.POINTER(C.c_float)))
+    p = pt.reshape(nt, 2).astype(np.float64)
+    if mod == 2:
+        c6, c12 = np.outer(p[:, 0], p[:, 0]), np.outer(p[:, 1], p[:, 1])
+    else:
+        sg = p[:, 0][:, None] + p[:, 0][None, :]
+        c6 = np.outer(p[:, 1], p[:, 1]) * sg**6
+        c12 = 2.0 * c6 * sg**6
+    np.testing.assert_allclose(c6, 6.0 * s.c6c12[..., 0], rtol=2e-6, atol=1e-12)
+    np.testing.assert_allclose(c12, 12.0 * s.c6c12[..., 1], rtol=2e-6, atol=1e-18)
+
+
+def test_grappa_flavour_vs_brute_force():
+    """Row f3: the Grappa kernel flavour -- tabulated Ewald + LB combination-rule LJ."""
+    s = systems.make("grappa1.5m", 3000)
+    on = O.OracleNonbonded(s)
+    on.search(s.x)
+    f, e, vir, _ = on.forces()
+    c = O.derive_consts(on.params)
+    fb, eb, vb = brute_force(s.x, s.q, s.type, s.c6c12, s.excl_offsets, s.excl_gids, s.box, c, "ewald", s.rc)
+    assert np.sqrt(((f - fb) ** 2).sum() / (fb**2).sum()) < 5e-6
+    assert abs(e[0] - eb[0]) / abs(eb[0]) < 1e-5
+    assert np.abs(vir - vb).max() / np.abs(vb).max() < 5e-6
