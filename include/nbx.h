@@ -279,6 +279,39 @@ NBX_API int nbx_halo_pack_x(const float* x_dev, const int32_t* idx_dev, int32_t 
 NBX_API int nbx_halo_unpack_add_f(float* f_dev, const int32_t* idx_dev, int32_t n,
                                   const float* in_dev, void* stream);
 
+/* ---- row f4: smooth particle-mesh Ewald and the leap-frog update --------------------- *
+ * The reciprocal-space half of the Ewald electrostatics whose real-space half is the
+ * EWALD / EWALD_TAB force kernel, as the reference's step submits it after the nonbonded
+ * kernels: KernelKind.PME_SPREAD, FFT_3D_FORWARD, PME_SOLVE, FFT_3D_INVERSE, PME_GATHER
+ * (costs.py:33-37, pipeline.py:241-246) and GRID_MEMSET (costs.py:42, pipeline.py:256-257).
+ * Algorithm and conventions: oracle/pme.py (Essmann et al. 1995, B-spline order 4, the
+ * same virial convention as the nonbonded path).  Rectangular boxes; one context per
+ * device, stream-ordered, not thread-safe; no CPU fallback.                              */
+typedef struct nbx_pme nbx_pme;
+typedef struct nbx_pme_params {
+    int32_t nk[3];  /* FFT grid (each even, >= 8; oracle/pme.py grid_dims: spacing 0.12 nm) */
+    int32_t order;  /* B-spline interpolation order: 4 (GROMACS GPU PME)                   */
+    float beta;     /* Ewald splitting coefficient, the real-space kernel's (nbx_consts)   */
+    float epsfac;   /* 138.935458 / epsilon_r                                              */
+} nbx_pme_params;
+
+NBX_API int nbx_pme_create(int device, const nbx_pme_params* p, nbx_pme** out);
+NBX_API int nbx_pme_destroy(nbx_pme* pme);
+NBX_API int nbx_pme_set_box(nbx_pme* pme, const float box[3]);
+/* Reciprocal-space forces of n charges: f[3a..3a+2] += F_a (device arrays, x and f as
+ * [n][3] floats, q as [n]).  flags: NBX_FORCE_ENERGY / NBX_FORCE_VIRIAL accumulate the
+ * reciprocal energy / virial into the context (read with nbx_pme_energy).                */
+NBX_API int nbx_pme_compute(nbx_pme* pme, int32_t n, const float* x_dev, const float* q_dev, float* f_dev,
+                            uint32_t flags, void* stream);
+/* Reads and clears the accumulated energy and virial (row-major 3x3); syncs `stream`.   */
+NBX_API int nbx_pme_energy(nbx_pme* pme, double* e_host, double* virial_host, void* stream);
+NBX_API int64_t nbx_pme_launch_count(nbx_pme* pme);
+
+/* Leap-frog update (KernelKind.LEAP_FROG, costs.py:39, pipeline.py:249-251), no
+ * constraints: v += f inv_mass dt; x += v dt (device arrays, [n][3] floats).            */
+NBX_API int nbx_leapfrog(int32_t n, float* x_dev, float* v_dev, const float* f_dev, const float* inv_mass_dev,
+                         float dt, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -740,4 +740,96 @@ NBX_API int nbx_halo_unpack_add_f(float* f, const int32_t* idx, int32_t n, const
     NBX_GUARD_END
 }
 
+// ---- row f4: PME and the leap-frog update (pme.cu) --------------------------------------
+NBX_API int nbx_pme_create(int device, const nbx_pme_params* p, nbx_pme** out)
+{
+    NBX_GUARD_BEGIN
+    if (!p || !out) return fail(NBX_EINVAL, "null argument");
+    *out = nullptr;
+    if (p->order != 4) return fail(NBX_EINVAL, "PME interpolation order must be 4");
+    for (int d = 0; d < 3; d++)
+        if (p->nk[d] < 8 || (p->nk[d] & 1)) return fail(NBX_EINVAL, "PME grid sizes must be even and >= 8");
+    if (!(p->beta > 0.0f) || !(p->epsfac > 0.0f)) return fail(NBX_EINVAL, "PME beta and epsfac must be positive");
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev <= device || device < 0)
+        return fail(NBX_ECUDA, std::string("no CUDA device ") + std::to_string(device) + " (" +
+                                   cudaGetErrorString(e) + "); libnbx has no CPU fallback");
+    cudaDeviceProp prop;
+    NBX_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+        return fail(NBX_ECUDA, std::string("device ") + prop.name + " is not sm_100 (built for sm_100a only)");
+    NBX_CUDA(cudaSetDevice(device));
+    nbx_pme* pme = new nbx_pme();
+    pme->device = device;
+    for (int d = 0; d < 3; d++) pme->nk[d] = p->nk[d];
+    pme->beta = p->beta;
+    pme->epsfac = p->epsfac;
+    try {
+        pme_setup(pme);
+    } catch (...) {
+        pme_release(pme);
+        delete pme;
+        throw;
+    }
+    *out = pme;
+    return NBX_OK;
+    NBX_GUARD_END
+}
+
+NBX_API int nbx_pme_destroy(nbx_pme* pme)
+{
+    NBX_GUARD_BEGIN
+    if (!pme) return NBX_OK;
+    cudaSetDevice(pme->device);
+    pme_release(pme);
+    delete pme;
+    return NBX_OK;
+    NBX_GUARD_END
+}
+
+NBX_API int nbx_pme_set_box(nbx_pme* pme, const float box[3])
+{
+    NBX_GUARD_BEGIN
+    NBX_CHECK_CTX(pme);
+    if (!box) return fail(NBX_EINVAL, "null box");
+    for (int d = 0; d < 3; d++)
+        if (!(box[d] > 0.0f)) return fail(NBX_EINVAL, "box edges must be positive");
+    pme_set_box(pme, box);
+    return NBX_OK;
+    NBX_GUARD_END
+}
+
+NBX_API int nbx_pme_compute(nbx_pme* pme, int32_t n, const float* x, const float* q, float* f, uint32_t flags,
+                            void* stream)
+{
+    NBX_GUARD_BEGIN
+    NBX_CHECK_CTX(pme);
+    if (!pme->have_box) return fail(NBX_EINVAL, "PME compute before set_box");
+    if (n < 0 || (n > 0 && (!x || !q || !f))) return fail(NBX_EINVAL, "bad PME arguments");
+    pme_compute(pme, n, x, q, f, flags, (cudaStream_t)stream);
+    return NBX_OK;
+    NBX_GUARD_END
+}
+
+NBX_API int nbx_pme_energy(nbx_pme* pme, double* e_host, double* virial_host, void* stream)
+{
+    NBX_GUARD_BEGIN
+    NBX_CHECK_CTX(pme);
+    pme_energy(pme, e_host, virial_host, (cudaStream_t)stream);
+    return NBX_OK;
+    NBX_GUARD_END
+}
+
+NBX_API int64_t nbx_pme_launch_count(nbx_pme* pme) { return pme ? pme->launches : -1; }
+
+NBX_API int nbx_leapfrog(int32_t n, float* x, float* v, const float* f, const float* inv_mass, float dt, void* stream)
+{
+    NBX_GUARD_BEGIN
+    if (n < 0 || (n > 0 && (!x || !v || !f || !inv_mass))) return fail(NBX_EINVAL, "bad leap-frog arguments");
+    leapfrog(n, x, v, f, inv_mass, dt, (cudaStream_t)stream);
+    return NBX_OK;
+    NBX_GUARD_END
+}
+
 } // extern "C"

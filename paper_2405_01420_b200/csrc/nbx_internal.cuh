@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <cufft.h>
 #include <stdint.h>
 
 #include <string>
@@ -144,6 +145,21 @@ struct nbx_ctx {
     cudaStream_t cap_stream = nullptr;
 };
 
+// PME context (row f4; pme.cu)
+struct nbx_pme {
+    int device = 0;
+    int nk[3] = {0, 0, 0};
+    float beta = 0.f, epsfac = 0.f;
+    float box[3] = {0.f, 0.f, 0.f};
+    bool have_box = false;
+    nbx::DBuf<float> grid;    // real grid [nx][ny][nz]: charges, then the potential
+    nbx::DBuf<float2> spec;   // half spectrum [nx][ny][nz/2+1]
+    nbx::DBuf<float> bmod;    // |b(m)|^2: [nx] then [ny] then [nz/2+1]
+    nbx::DBuf<double> acc;    // [0] energy, [1..9] virial
+    cufftHandle fwd = 0, inv = 0;
+    int64_t launches = 0;
+};
+
 namespace nbx {
 
 // ---- shared device helpers ------------------------------------------------------------
@@ -199,5 +215,11 @@ void peer_force_nonlocal(nbx_ctx* ctx, unsigned seq, cudaStream_t st);
 void peer_get_f(nbx_ctx* ctx, float* f, unsigned seq, cudaStream_t st);
 int peer_status(nbx_ctx* ctx);
 ForceConsts make_force_consts(const nbx_consts& c);
+void pme_setup(nbx_pme* pme);
+void pme_set_box(nbx_pme* pme, const float box[3]);
+void pme_compute(nbx_pme* pme, int n, const float* x, const float* q, float* f, unsigned flags, cudaStream_t st);
+void pme_energy(nbx_pme* pme, double* e, double* vir, cudaStream_t st);
+void pme_release(nbx_pme* pme);
+void leapfrog(int n, float* x, float* v, const float* f, const float* inv_mass, float dt, cudaStream_t st);
 
 } // namespace nbx

@@ -68,7 +68,9 @@ EXPORTS = ["nbx_last_error", "nbx_version", "nbx_derive_consts", "nbx_ewald_tabl
            "nbx_grid_info_get", "nbx_grid_export", "nbx_list_sizes_get", "nbx_list_export",
            "nbx_count_pairs", "nbx_fma_peak", "nbx_launch_count", "nbx_halo_pack_x", "nbx_halo_unpack_add_f",
            "nbx_peer_init", "nbx_peer_open", "nbx_peer_set_halo", "nbx_peer_put_x", "nbx_peer_halo_x",
-           "nbx_peer_force_nonlocal", "nbx_peer_get_f", "nbx_peer_status"]
+           "nbx_peer_force_nonlocal", "nbx_peer_get_f", "nbx_peer_status",
+           "nbx_pme_create", "nbx_pme_destroy", "nbx_pme_set_box", "nbx_pme_compute", "nbx_pme_energy",
+           "nbx_pme_launch_count", "nbx_leapfrog"]
 
 _lib = None
 
@@ -117,6 +119,14 @@ def lib():
         L.nbx_peer_force_nonlocal.argtypes = [vp, u32, vp]
         L.nbx_peer_get_f.argtypes = [vp, vp, u32, vp]
         L.nbx_peer_status.argtypes = [vp, vp]
+        L.nbx_pme_create.argtypes = [C.c_int, vp, C.POINTER(vp)]
+        L.nbx_pme_destroy.argtypes = [vp]
+        L.nbx_pme_set_box.argtypes = [vp, vp]
+        L.nbx_pme_compute.argtypes = [vp, i32, vp, vp, vp, u32, vp]
+        L.nbx_pme_energy.argtypes = [vp, vp, vp, vp]
+        L.nbx_pme_launch_count.argtypes = [vp]
+        L.nbx_pme_launch_count.restype = C.c_int64
+        L.nbx_leapfrog.argtypes = [i32, vp, vp, vp, vp, C.c_float, vp]
         _lib = L
     return _lib
 

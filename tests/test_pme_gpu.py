@@ -1,0 +1,89 @@
+"""Row f4 on the GPU: the sm_100a PME (spread / cuFFT / solve / gather, pme.cu) against the
+float64 oracle restatement (oracle/pme.py) on identical inputs and grids, through the C-ABI;
+and the leap-frog update.  The bar for PME is looser than the nonbonded one because the
+charge grid is accumulated and transformed in fp32: forces rel RMS <= 2e-5, energy and
+virial rel <= 1e-5 (the fp32 grid/FFT limit; the oracle's own grid error at these settings
+is ~1e-4, tests/test_pme_oracle.py)."""
+import numpy as np
+import pytest
+
+from oracle import pme as P
+from paper_2405_01420_b200 import systems
+
+pytestmark = pytest.mark.gpu
+
+FTOL, ETOL = 2e-5, 1e-5
+
+
+def _dev(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a, np.float32)).cuda()
+
+
+@pytest.mark.parametrize("config,natoms", [("rnase24k", None), ("water12m", 30000), ("stmv", 200000)])
+def test_pme_matches_oracle(gpu, config, natoms):
+    import torch
+    from paper_2405_01420_b200 import pme
+    s = systems.make(config, natoms)
+    pm = pme.Pme.for_system(s)
+    x, q = _dev(s.x), _dev(s.q)
+    f, (e, vir) = pm.compute(x, q, energy=True, virial=True)
+    f2 = pm.compute(x, q)  # force-only call gives the same forces
+    torch.cuda.synchronize()
+    Eo, fo, vo = P.pme(s.x, s.q, s.box, pm_beta(s), 138.935458, pm.nk, 4)
+    fg = f.cpu().numpy().astype(np.float64)
+    rel = np.sqrt(((fg - fo) ** 2).sum() / (fo**2).sum())
+    assert rel <= FTOL, rel
+    assert np.sqrt(((f2.cpu().numpy() - fo) ** 2).sum() / (fo**2).sum()) <= FTOL
+    assert abs(e - Eo) / abs(Eo) <= ETOL, (e, Eo)
+    assert np.abs(vir - vo).max() / np.abs(vo).max() <= ETOL
+    assert pm.launch_count() >= 6
+
+
+def pm_beta(s):
+    from paper_2405_01420_b200 import nbx
+    return float(nbx.derive_consts(nbx.make_params(**s.params()))["beta"])
+
+
+def test_pme_accumulates_and_moves(gpu):
+    """out= accumulates; coordinates outside the box (several images away) give the same
+    forces as wrapped ones."""
+    import torch
+    from paper_2405_01420_b200 import pme
+    s = systems.make("rnase24k", 3000)
+    pm = pme.Pme.for_system(s)
+    x, q = _dev(s.x), _dev(s.q)
+    f1 = pm.compute(x, q)
+    f = torch.ones_like(x)
+    pm.compute(x, q, out=f)
+    torch.testing.assert_close(f, f1 + 1.0, rtol=1e-5, atol=1e-3)  # fp32 atomics: order-dependent
+    shift = np.array([2, -3, 1], dtype=np.float32) * s.box
+    f3 = pm.compute(_dev(s.x + shift), q)
+    torch.cuda.synchronize()
+    rel = float((f3 - f1).norm() / f1.norm())
+    assert rel < 1e-4, rel
+
+
+def test_pme_rejects_bad_parameters(gpu):
+    from paper_2405_01420_b200 import nbx, pme
+    with pytest.raises(nbx.NbxError):
+        pme.Pme([3.0, 3.0, 3.0], 3.0, nk=(25, 24, 24))
+    with pytest.raises(nbx.NbxError):
+        pme.Pme([3.0, 3.0, 3.0], 3.0, order=5)
+    with pytest.raises(ValueError):
+        pme.Pme.for_system(systems.make("water3k"))  # reaction field: no PME
+
+
+def test_leapfrog(gpu):
+    import torch
+    from paper_2405_01420_b200 import pme
+    rng = np.random.default_rng(3)
+    n = 1000
+    x, v, f = (rng.standard_normal((n, 3)).astype(np.float32) for _ in range(3))
+    im = rng.uniform(0.05, 1.0, n).astype(np.float32)
+    xd, vd, fd, imd = _dev(x), _dev(v), _dev(f), _dev(im)
+    pme.leapfrog(xd, vd, fd, imd, 0.002)
+    torch.cuda.synchronize()
+    vn = v + f * im[:, None] * np.float32(0.002)
+    np.testing.assert_allclose(vd.cpu().numpy(), vn, rtol=1e-6, atol=1e-6)
+    np.testing.assert_allclose(xd.cpu().numpy(), x + vn * np.float32(0.002), rtol=1e-6, atol=1e-6)

@@ -12,10 +12,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "scratch", "variants")
 VARIANTS = {
     "base": [],
-    "ri6": ["-DNBX_RI6=1"],
-    "pred": ["-DNBX_PREDACC=1"],
-    "ewn5": ["-DNBX_EWN5=1"],
-    "all3": ["-DNBX_RI6=1", "-DNBX_PREDACC=1", "-DNBX_EWN5=1"],
+    "eacc64": ["-DNBX_EACC_F32=0"],
 }
 
 
@@ -32,7 +29,7 @@ def build():
             subprocess.check_call(cmd, stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
             objs.append(o)
         subprocess.check_call([B._nvcc(), *B.ARCH, "-shared", "-o", os.path.join(OUT, f"libnbx_{name}.so"), *objs,
-                               "-lcudart"])
+                               "-lcudart", "-lcufft"])
         print("built", name)
 
 
