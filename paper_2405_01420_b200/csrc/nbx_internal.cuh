@@ -155,6 +155,7 @@ struct nbx_pme {
     nbx::DBuf<float> grid;    // real grid [nx][ny][nz]: charges, then the potential
     nbx::DBuf<float2> spec;   // half spectrum [nx][ny][nz/2+1]
     nbx::DBuf<float> bmod;    // |b(m)|^2: [nx] then [ny] then [nz/2+1]
+    nbx::DBuf<float> gex;     // exp(-pi^2 mt_d^2 / beta^2), same layout (set_box)
     nbx::DBuf<double> acc;    // [0] energy, [1..9] virial
     cufftHandle fwd = 0, inv = 0;
     int64_t launches = 0;

@@ -6,17 +6,19 @@
 // (pipeline.py:249-251).  Algorithm and conventions: oracle/pme.py (its docstring is the spec).
 //
 // sm_100a design:
-//  * spread / gather: 16 threads per atom (one (y, z) spline pair each, the 4 x points in a
+//  * spread / gather: 4 threads per atom (one z spline point each, the 16 (x, y) points in a
 //    loop), so 4 adjacent threads touch 4 consecutive z points; charges are added with
-//    red.global.add.f32 into the L2-resident grid (the 12M-atom grid, 420^3 fp32 = 296 MB,
-//    streams through L2 in the input's spatial order); gather reduces the 16 partial forces
-//    with 4 xor shuffles;
-//  * the B-spline weights are recomputed in each kernel (about 60 flops per thread) instead of
-//    stored: 96 bytes per atom of HBM traffic saved twice;
+//    red.global.add.f32 into the grid (the 12M-atom grid, 420^3 fp32 = 296 MB, streams
+//    through L2 in the input's spatial order); gather reduces the 4 partial forces with 2 xor
+//    shuffles (16 threads per atom, measured first, spent most of their time recomputing the
+//    B-spline weights: spread 1.50 / gather 2.11 ms on 12 M atoms);
+//  * the B-spline weights are recomputed in each kernel instead of stored: 96 bytes per atom
+//    of HBM traffic saved twice;
 //  * FFTs: cuFFT single-precision R2C / C2R plans, unnormalised, out of place (library call,
 //    like cuBLAS for a plain GEMM);
-//  * solve: one thread per half-spectrum element, influence function from per-dimension
-//    modulus tables, fp64 block reduction of the energy and virial (energy steps only);
+//  * solve: one thread per half-spectrum element on a 3-D launch grid, influence function from
+//    per-dimension modulus and Gaussian tables, fp64 block reduction of the energy and virial
+//    (energy steps only);
 //  * no CPU fallback: the context refuses to exist without an sm_100 device (capi.cu).
 #include <cmath>
 #include <vector>
@@ -68,12 +70,14 @@ __device__ __forceinline__ float sel4(const float v[4], int j)
     return j == 0 ? v[0] : (j == 1 ? v[1] : (j == 2 ? v[2] : v[3]));
 }
 
+// 4 threads per atom (one z spline point each, 16 (x, y) points in a loop): 4 adjacent threads
+// add into 4 consecutive z points, and the B-spline weights are computed 4x per atom, not 16x
 __global__ void __launch_bounds__(PME_THREADS) k_pme_spread(int n, const float* __restrict__ x,
                                                             const float* __restrict__ q, PmeGeom g,
                                                             float* __restrict__ grid)
 {
-    const int a = (blockIdx.x * PME_THREADS + threadIdx.x) >> 4;
-    const int t = threadIdx.x & 15, jy = t >> 2, jz = t & 3;
+    const int a = (blockIdx.x * PME_THREADS + threadIdx.x) >> 2;
+    const int jz = threadIdx.x & 3;
     if (a >= n) return;
     const float qa = q[a];
     if (qa == 0.0f) return;
@@ -85,37 +89,39 @@ __global__ void __launch_bounds__(PME_THREADS) k_pme_spread(int n, const float* 
     bspline4(wx, tx, d);
     bspline4(wy, ty, d);
     bspline4(wz, tz, d);
-    const float qyz = qa * sel4(ty, jy) * sel4(tz, jz);
-    const int y = wrapk(iy - jy, g.ny), z = wrapk(iz - jz, g.nz);
-    float* row = grid + (size_t)y * g.nz + z;
+    const float qz = qa * sel4(tz, jz);
+    float* col = grid + wrapk(iz - jz, g.nz);
 #pragma unroll
     for (int jx = 0; jx < 4; jx++) {
-        const int xx = wrapk(ix - jx, g.nx);
-        atomicAdd(row + (size_t)xx * g.ny * g.nz, qyz * tx[jx]);
+        float* plane = col + (size_t)wrapk(ix - jx, g.nx) * g.ny * g.nz;
+        const float qxz = qz * tx[jx];
+#pragma unroll
+        for (int jy = 0; jy < 4; jy++) atomicAdd(plane + (size_t)wrapk(iy - jy, g.ny) * g.nz, qxz * ty[jy]);
     }
 }
 
+// one thread per half-spectrum element on a (z, y, x) launch grid (no index divisions); the
+// Gaussian factor is a product of per-dimension tables: G = ex[x] ey[y] ez[z] / (pi V m^2) b
 __global__ void __launch_bounds__(256) k_pme_solve(PmeGeom g, float beta, float epsfac, float2* __restrict__ spec,
-                                                   const float* __restrict__ bmod, int energy, double* acc)
+                                                   const float* __restrict__ bmod, const float* __restrict__ gex,
+                                                   int energy, double* acc)
 {
     const int nzh = g.nz / 2 + 1;
-    const long long total = (long long)g.nx * g.ny * nzh;
-    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int z = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y, xi = blockIdx.z;
     double ev[7] = {0, 0, 0, 0, 0, 0, 0}; // E, xx, yy, zz, xy, xz, yz
-    if (e < total) {
-        const int z = (int)(e % nzh);
-        const int y = (int)((e / nzh) % g.ny);
-        const int xi = (int)(e / ((long long)nzh * g.ny));
+    if (z < nzh) {
+        const long long e = ((long long)xi * g.ny + y) * nzh + z;
         const int mx = xi <= g.nx / 2 ? xi : xi - g.nx;
         const int my = y <= g.ny / 2 ? y : y - g.ny;
         const float tx = (float)mx * g.ibx, ty = (float)my * g.iby, tz = (float)z * g.ibz;
         const float m2 = tx * tx + ty * ty + tz * tz;
-        float G = 0.0f;
         const float pi = 3.14159265358979f;
-        const float vol = g.bx * g.by * g.bz;
+        float G = 0.0f;
         if (e != 0) {
             const float b = bmod[xi] * bmod[g.nx + y] * bmod[g.nx + g.ny + z];
-            G = expf(-pi * pi * m2 / (beta * beta)) / (pi * vol * m2) * b;
+            const float ex = gex[xi] * gex[g.nx + y] * gex[g.nx + g.ny + z];
+            G = __fdividef(ex * b, pi * (g.bx * g.by * g.bz) * m2);
         }
         float2 s = spec[e];
         if (energy && e != 0) {
@@ -152,12 +158,13 @@ __global__ void __launch_bounds__(256) k_pme_solve(PmeGeom g, float beta, float 
     }
 }
 
+// 4 threads per atom (one z spline point each, 16 (x, y) points), 2 xor shuffles
 __global__ void __launch_bounds__(PME_THREADS) k_pme_gather(int n, const float* __restrict__ x,
                                                             const float* __restrict__ q, PmeGeom g, float epsfac,
                                                             const float* __restrict__ phi, float* __restrict__ f)
 {
-    const int a = (blockIdx.x * PME_THREADS + threadIdx.x) >> 4;
-    const int t = threadIdx.x & 15, jy = t >> 2, jz = t & 3;
+    const int a = (blockIdx.x * PME_THREADS + threadIdx.x) >> 2;
+    const int jz = threadIdx.x & 3;
     const bool live = a < n;
     const int ac = live ? a : n - 1;
     const float qa = q[ac];
@@ -169,26 +176,34 @@ __global__ void __launch_bounds__(PME_THREADS) k_pme_gather(int n, const float* 
     bspline4(wx, tx, dx);
     bspline4(wy, ty, dy);
     bspline4(wz, tz, dz);
-    const int y = wrapk(iy - jy, g.ny), z = wrapk(iz - jz, g.nz);
-    const float* row = phi + (size_t)y * g.nz + z;
-    const float ty1 = sel4(ty, jy), tz1 = sel4(tz, jz), dy1 = sel4(dy, jy), dz1 = sel4(dz, jz);
-    const float tyz = ty1 * tz1, dyz = dy1 * tz1, tdz = ty1 * dz1;
+    const float tz1 = sel4(tz, jz), dz1 = sel4(dz, jz);
+    const float* col = phi + wrapk(iz - jz, g.nz);
     float sx = 0.f, sy = 0.f, sz = 0.f;
 #pragma unroll
     for (int jx = 0; jx < 4; jx++) {
-        const int xx = wrapk(ix - jx, g.nx);
-        const float p = __ldg(row + (size_t)xx * g.ny * g.nz);
-        sx = fmaf(dx[jx] * tyz, p, sx);
-        sy = fmaf(tx[jx] * dyz, p, sy);
-        sz = fmaf(tx[jx] * tdz, p, sz);
-    }
+        const float* plane = col + (size_t)wrapk(ix - jx, g.nx) * g.ny * g.nz;
+        float px = 0.f, py = 0.f, pz = 0.f; // sums over y at fixed x
 #pragma unroll
-    for (int o = 8; o > 0; o >>= 1) {
+        for (int jy = 0; jy < 4; jy++) {
+            const float p = __ldg(plane + (size_t)wrapk(iy - jy, g.ny) * g.nz);
+            px = fmaf(ty[jy], p, px);
+            py = fmaf(dy[jy], p, py);
+        }
+        pz = px;
+        sx = fmaf(dx[jx], px, sx);
+        sy = fmaf(tx[jx], py, sy);
+        sz = fmaf(tx[jx], pz, sz);
+    }
+    sx *= tz1;
+    sy *= tz1;
+    sz *= dz1;
+#pragma unroll
+    for (int o = 2; o > 0; o >>= 1) {
         sx += __shfl_xor_sync(0xffffffffu, sx, o);
         sy += __shfl_xor_sync(0xffffffffu, sy, o);
         sz += __shfl_xor_sync(0xffffffffu, sz, o);
     }
-    if (live && t == 0 && qa != 0.0f) {
+    if (live && jz == 0 && qa != 0.0f) {
         const float s = -epsfac * qa;
         f[3 * a + 0] += s * (float)g.nx * g.ibx * sx;
         f[3 * a + 1] += s * (float)g.ny * g.iby * sy;
@@ -232,6 +247,7 @@ void pme_setup(nbx_pme* pme)
     bsp_moduli(nz, b, nz / 2 + 1);
     pme->bmod.ensure(b.size());
     NBX_CUDA(cudaMemcpy(pme->bmod.p, b.data(), sizeof(float) * b.size(), cudaMemcpyHostToDevice));
+    pme->gex.ensure(b.size());
     pme->acc.ensure(10);
     NBX_CUDA(cudaMemset(pme->acc.p, 0, sizeof(double) * 10));
     if (cufftPlan3d(&pme->fwd, nx, ny, nz, CUFFT_R2C) != CUFFT_SUCCESS ||
@@ -243,6 +259,18 @@ void pme_set_box(nbx_pme* pme, const float box[3])
 {
     for (int d = 0; d < 3; d++) pme->box[d] = box[d];
     pme->have_box = true;
+    // per-dimension Gaussian factors exp(-pi^2 mt_d^2 / beta^2), mt_d = m_d / L_d (m_d signed)
+    std::vector<float> t;
+    const double pb = M_PI / (double)pme->beta;
+    for (int d = 0; d < 3; d++) {
+        const int K = pme->nk[d], cnt = d < 2 ? K : K / 2 + 1;
+        for (int m = 0; m < cnt; m++) {
+            const int ms = (d < 2 && m > K / 2) ? m - K : m;
+            const double mt = (double)ms / (double)box[d];
+            t.push_back((float)std::exp(-pb * pb * mt * mt));
+        }
+    }
+    NBX_CUDA(cudaMemcpy(pme->gex.p, t.data(), sizeof(float) * t.size(), cudaMemcpyHostToDevice));
 }
 
 static PmeGeom geom(const nbx_pme* pme)
@@ -264,9 +292,8 @@ void pme_compute(nbx_pme* pme, int n, const float* x, const float* q, float* f, 
 {
     const PmeGeom g = geom(pme);
     const size_t ng = (size_t)g.nx * g.ny * g.nz;
-    const long long nspec = (long long)g.nx * g.ny * (g.nz / 2 + 1);
     NBX_CUDA(cudaMemsetAsync(pme->grid.p, 0, sizeof(float) * ng, st)); // GRID_MEMSET
-    const int blocks = (int)(((long long)n * 16 + PME_THREADS - 1) / PME_THREADS);
+    const int blocks = (int)(((long long)n * 4 + PME_THREADS - 1) / PME_THREADS);
     if (n > 0) k_pme_spread<<<blocks, PME_THREADS, 0, st>>>(n, x, q, g, pme->grid.p);
     NBX_CUDA(cudaGetLastError());
     if (cufftSetStream(pme->fwd, st) != CUFFT_SUCCESS || cufftSetStream(pme->inv, st) != CUFFT_SUCCESS)
@@ -274,8 +301,10 @@ void pme_compute(nbx_pme* pme, int n, const float* x, const float* q, float* f, 
     if (cufftExecR2C(pme->fwd, pme->grid.p, reinterpret_cast<cufftComplex*>(pme->spec.p)) != CUFFT_SUCCESS)
         throw CudaError{cudaErrorLaunchFailure, "cufftExecR2C"};
     const int energy = (flags & (NBX_FORCE_ENERGY | NBX_FORCE_VIRIAL)) != 0;
-    k_pme_solve<<<(int)((nspec + 255) / 256), 256, 0, st>>>(g, pme->beta, pme->epsfac, pme->spec.p, pme->bmod.p,
-                                                           energy, pme->acc.p);
+    const int nzh = g.nz / 2 + 1;
+    const dim3 sgrid((nzh + 127) / 128, g.ny, g.nx);
+    k_pme_solve<<<sgrid, 128, 0, st>>>(g, pme->beta, pme->epsfac, pme->spec.p, pme->bmod.p, pme->gex.p, energy,
+                                       pme->acc.p);
     NBX_CUDA(cudaGetLastError());
     if (cufftExecC2R(pme->inv, reinterpret_cast<cufftComplex*>(pme->spec.p), pme->grid.p) != CUFFT_SUCCESS)
         throw CudaError{cudaErrorLaunchFailure, "cufftExecC2R"};
@@ -307,6 +336,7 @@ void pme_release(nbx_pme* pme)
     pme->grid.release();
     pme->spec.release();
     pme->bmod.release();
+    pme->gex.release();
     pme->acc.release();
 }
 
