@@ -306,6 +306,11 @@ NBX_API int nbx_pme_compute(nbx_pme* pme, int32_t n, const float* x_dev, const f
 /* Reads and clears the accumulated energy and virial (row-major 3x3); syncs `stream`.   */
 NBX_API int nbx_pme_energy(nbx_pme* pme, double* e_host, double* virial_host, void* stream);
 NBX_API int64_t nbx_pme_launch_count(nbx_pme* pme);
+/* One force-only nbx_pme_compute with CUDA events between its stages; ms_host[6] receives
+ * the per-stage times (GRID_MEMSET, PME_SPREAD, FFT_3D_FORWARD, PME_SOLVE, FFT_3D_INVERSE,
+ * PME_GATHER) for the reference's calibrate samples (costs_adapter.py).  Synchronises.   */
+NBX_API int nbx_pme_profile(nbx_pme* pme, int32_t n, const float* x_dev, const float* q_dev, float* f_dev,
+                            float* ms_host, void* stream);
 
 /* Leap-frog update (KernelKind.LEAP_FROG, costs.py:39, pipeline.py:249-251), no
  * constraints: v += f inv_mass dt; x += v dt (device arrays, [n][3] floats).            */

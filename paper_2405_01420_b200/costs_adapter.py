@@ -14,7 +14,9 @@ from __future__ import annotations
 
 from typing import Dict, List, Sequence, Tuple
 
-KINDS = ("nbnxm_local", "prune_only", "pair_search", "reduce_forces")
+KINDS = ("nbnxm_local", "prune_only", "pair_search", "reduce_forces",
+         # row f4: the PME stages and the update (pipeline.py:241-257), from nbx_pme_profile
+         "grid_memset", "pme_spread", "fft_3d_forward", "pme_solve", "fft_3d_inverse", "pme_gather", "leap_frog")
 
 
 def fit_affine(points: Sequence[Tuple[int, float]], clamp_floor: bool = True) -> Tuple[float, float]:
@@ -72,7 +74,8 @@ def parse_cfg(text: str) -> Dict[str, List[Tuple[int, float]]]:
 
 
 def measure(sizes=(24000, 96000, 384000), reps=20, coulomb="ewald", device=0):
-    """Time the four kernels on water boxes of the given atom counts (CUDA events)."""
+    """Time the NB kernels, the PME stages and the update on water boxes of the given atom
+    counts (CUDA events)."""
     import torch
 
     from . import nbx, systems
@@ -102,6 +105,19 @@ def measure(sizes=(24000, 96000, 384000), reps=20, coulomb="ewald", device=0):
         samples["reduce_forces"].append((s.natoms, timed(lambda: nb.get_f(f))))
         samples["pair_search"].append((s.natoms, timed(lambda: nb.search(x), r=max(2, reps // 5))))
         nb.close()
+        from . import pme
+        pm = pme.Pme.for_system(s, device=device)
+        q = torch.from_numpy(s.q).cuda(device)
+        pm.profile(x, q, out=f)  # warm-up (plans, caches)
+        acc = {k: 0.0 for k in pm.STAGES}
+        for _ in range(reps):
+            for k, v in pm.profile(x, q, out=f).items():
+                acc[k] += v
+        for k in pm.STAGES:
+            samples[k].append((s.natoms, acc[k] * 1e6 / reps))
+        v = torch.zeros_like(x)
+        im = torch.ones_like(q)
+        samples["leap_frog"].append((s.natoms, timed(lambda: pme.leapfrog(x, v, f, im, 0.0))))
     return samples
 
 

@@ -823,6 +823,18 @@ NBX_API int nbx_pme_energy(nbx_pme* pme, double* e_host, double* virial_host, vo
 
 NBX_API int64_t nbx_pme_launch_count(nbx_pme* pme) { return pme ? pme->launches : -1; }
 
+NBX_API int nbx_pme_profile(nbx_pme* pme, int32_t n, const float* x, const float* q, float* f, float* ms_host,
+                            void* stream)
+{
+    NBX_GUARD_BEGIN
+    NBX_CHECK_CTX(pme);
+    if (!pme->have_box) return fail(NBX_EINVAL, "PME profile before set_box");
+    if (!ms_host || n < 0 || (n > 0 && (!x || !q || !f))) return fail(NBX_EINVAL, "bad PME arguments");
+    pme_profile(pme, n, x, q, f, ms_host, (cudaStream_t)stream);
+    return NBX_OK;
+    NBX_GUARD_END
+}
+
 NBX_API int nbx_leapfrog(int32_t n, float* x, float* v, const float* f, const float* inv_mass, float dt, void* stream)
 {
     NBX_GUARD_BEGIN

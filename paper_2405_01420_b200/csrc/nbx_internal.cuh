@@ -218,7 +218,9 @@ int peer_status(nbx_ctx* ctx);
 ForceConsts make_force_consts(const nbx_consts& c);
 void pme_setup(nbx_pme* pme);
 void pme_set_box(nbx_pme* pme, const float box[3]);
-void pme_compute(nbx_pme* pme, int n, const float* x, const float* q, float* f, unsigned flags, cudaStream_t st);
+void pme_compute(nbx_pme* pme, int n, const float* x, const float* q, float* f, unsigned flags, cudaStream_t st,
+                 cudaEvent_t* ev = nullptr);
+void pme_profile(nbx_pme* pme, int n, const float* x, const float* q, float* f, float ms[6], cudaStream_t st);
 void pme_energy(nbx_pme* pme, double* e, double* vir, cudaStream_t st);
 void pme_release(nbx_pme* pme);
 void leapfrog(int n, float* x, float* v, const float* f, const float* inv_mass, float dt, cudaStream_t st);

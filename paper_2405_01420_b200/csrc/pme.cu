@@ -288,29 +288,49 @@ static PmeGeom geom(const nbx_pme* pme)
     return g;
 }
 
-void pme_compute(nbx_pme* pme, int n, const float* x, const float* q, float* f, unsigned flags, cudaStream_t st)
+// ev (optional, 7 events): recorded before the memset and after each of the 6 stages
+// (memset, spread, R2C, solve, C2R, gather) -- nbx_pme_profile's per-stage times
+void pme_compute(nbx_pme* pme, int n, const float* x, const float* q, float* f, unsigned flags, cudaStream_t st,
+                 cudaEvent_t* ev)
 {
     const PmeGeom g = geom(pme);
     const size_t ng = (size_t)g.nx * g.ny * g.nz;
+    if (ev) NBX_CUDA(cudaEventRecord(ev[0], st));
     NBX_CUDA(cudaMemsetAsync(pme->grid.p, 0, sizeof(float) * ng, st)); // GRID_MEMSET
+    if (ev) NBX_CUDA(cudaEventRecord(ev[1], st));
     const int blocks = (int)(((long long)n * 4 + PME_THREADS - 1) / PME_THREADS);
     if (n > 0) k_pme_spread<<<blocks, PME_THREADS, 0, st>>>(n, x, q, g, pme->grid.p);
     NBX_CUDA(cudaGetLastError());
+    if (ev) NBX_CUDA(cudaEventRecord(ev[2], st));
     if (cufftSetStream(pme->fwd, st) != CUFFT_SUCCESS || cufftSetStream(pme->inv, st) != CUFFT_SUCCESS)
         throw CudaError{cudaErrorInvalidValue, "cufftSetStream"};
     if (cufftExecR2C(pme->fwd, pme->grid.p, reinterpret_cast<cufftComplex*>(pme->spec.p)) != CUFFT_SUCCESS)
         throw CudaError{cudaErrorLaunchFailure, "cufftExecR2C"};
+    if (ev) NBX_CUDA(cudaEventRecord(ev[3], st));
     const int energy = (flags & (NBX_FORCE_ENERGY | NBX_FORCE_VIRIAL)) != 0;
     const int nzh = g.nz / 2 + 1;
     const dim3 sgrid((nzh + 127) / 128, g.ny, g.nx);
     k_pme_solve<<<sgrid, 128, 0, st>>>(g, pme->beta, pme->epsfac, pme->spec.p, pme->bmod.p, pme->gex.p, energy,
                                        pme->acc.p);
     NBX_CUDA(cudaGetLastError());
+    if (ev) NBX_CUDA(cudaEventRecord(ev[4], st));
     if (cufftExecC2R(pme->inv, reinterpret_cast<cufftComplex*>(pme->spec.p), pme->grid.p) != CUFFT_SUCCESS)
         throw CudaError{cudaErrorLaunchFailure, "cufftExecC2R"};
+    if (ev) NBX_CUDA(cudaEventRecord(ev[5], st));
     if (n > 0) k_pme_gather<<<blocks, PME_THREADS, 0, st>>>(n, x, q, g, pme->epsfac, pme->grid.p, f);
     NBX_CUDA(cudaGetLastError());
+    if (ev) NBX_CUDA(cudaEventRecord(ev[6], st));
     pme->launches += (n > 0 ? 3 : 1);
+}
+
+void pme_profile(nbx_pme* pme, int n, const float* x, const float* q, float* f, float ms[6], cudaStream_t st)
+{
+    cudaEvent_t ev[7];
+    for (int k = 0; k < 7; k++) NBX_CUDA(cudaEventCreate(&ev[k]));
+    pme_compute(pme, n, x, q, f, 0u, st, ev);
+    NBX_CUDA(cudaEventSynchronize(ev[6]));
+    for (int k = 0; k < 6; k++) NBX_CUDA(cudaEventElapsedTime(&ms[k], ev[k], ev[k + 1]));
+    for (int k = 0; k < 7; k++) cudaEventDestroy(ev[k]);
 }
 
 void pme_energy(nbx_pme* pme, double* e, double* vir, cudaStream_t st)

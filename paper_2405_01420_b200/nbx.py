@@ -70,7 +70,7 @@ EXPORTS = ["nbx_last_error", "nbx_version", "nbx_derive_consts", "nbx_ewald_tabl
            "nbx_peer_init", "nbx_peer_open", "nbx_peer_set_halo", "nbx_peer_put_x", "nbx_peer_halo_x",
            "nbx_peer_force_nonlocal", "nbx_peer_get_f", "nbx_peer_status",
            "nbx_pme_create", "nbx_pme_destroy", "nbx_pme_set_box", "nbx_pme_compute", "nbx_pme_energy",
-           "nbx_pme_launch_count", "nbx_leapfrog"]
+           "nbx_pme_launch_count", "nbx_pme_profile", "nbx_leapfrog"]
 
 _lib = None
 
@@ -126,6 +126,7 @@ def lib():
         L.nbx_pme_energy.argtypes = [vp, vp, vp, vp]
         L.nbx_pme_launch_count.argtypes = [vp]
         L.nbx_pme_launch_count.restype = C.c_int64
+        L.nbx_pme_profile.argtypes = [vp, i32, vp, vp, vp, vp, vp]
         L.nbx_leapfrog.argtypes = [i32, vp, vp, vp, vp, C.c_float, vp]
         _lib = L
     return _lib

@@ -90,6 +90,19 @@ class Pme:
                                            C.c_void_p(st)))
         return f, (float(e[0]), v.reshape(3, 3))
 
+    STAGES = ("grid_memset", "pme_spread", "fft_3d_forward", "pme_solve", "fft_3d_inverse", "pme_gather")
+
+    def profile(self, x, q, out=None):
+        """Per-stage milliseconds of one force-only evaluation (reference KernelKind names)."""
+        import torch
+        f = torch.zeros_like(x) if out is None else out
+        ms = np.zeros(6, dtype=np.float32)
+        nbx.check(nbx.lib().nbx_pme_profile(self.h, int(x.shape[0]), C.c_void_p(x.data_ptr()),
+                                            C.c_void_p(q.data_ptr()), C.c_void_p(f.data_ptr()),
+                                            ms.ctypes.data_as(C.c_void_p),
+                                            C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+        return dict(zip(self.STAGES, (float(v) for v in ms)))
+
     def launch_count(self):
         return int(nbx.lib().nbx_pme_launch_count(self.h))
 

@@ -87,3 +87,19 @@ def test_leapfrog(gpu):
     vn = v + f * im[:, None] * np.float32(0.002)
     np.testing.assert_allclose(vd.cpu().numpy(), vn, rtol=1e-6, atol=1e-6)
     np.testing.assert_allclose(xd.cpu().numpy(), x + vn * np.float32(0.002), rtol=1e-6, atol=1e-6)
+
+
+def test_pme_profile_stages(gpu):
+    """nbx_pme_profile: one evaluation with per-stage times under the reference's kernel kinds
+    (pipeline.py:241-257); forces as from compute."""
+    import torch
+    from paper_2405_01420_b200 import pme
+    s = systems.make("rnase24k")
+    pm = pme.Pme.for_system(s)
+    x, q = _dev(s.x), _dev(s.q)
+    f = torch.zeros_like(x)
+    ms = pm.profile(x, q, out=f)
+    assert set(ms) == set(pme.Pme.STAGES) and all(v >= 0.0 for v in ms.values())
+    f2 = pm.compute(x, q)
+    torch.cuda.synchronize()
+    assert float((f - f2).norm() / f2.norm()) < 1e-5

@@ -38,10 +38,12 @@ def main():
         torch.cuda.synchronize()
         t2 = time.perf_counter()
         runs.append((1e3 * (t1 - t0), 1e3 * (t2 - t1), dict(d.timing)))
-    if rank == 0:
-        for tr, ts, tim in runs:
-            print(f"repartition {tr:.2f} ms, first step after {ts:.2f} ms: "
-                  + ", ".join(f"{k} {1e3 * v:.2f}" for k, v in tim.items()))
+    for r in range(world):
+        dist.barrier()
+        if rank == r:
+            for tr, ts, tim in runs[-2:]:
+                print(f"rank {rank}: repartition {tr:.2f} ms, first step after {ts:.2f} ms: "
+                      + ", ".join(f"{k} {1e3 * v:.2f}" for k, v in tim.items()), flush=True)
     dist.destroy_process_group()
 
 
