@@ -12,7 +12,6 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "scratch", "variants")
 VARIANTS = {
     "base": [],
-    "eacc64": ["-DNBX_EACC_F32=0"],
 }
 
 

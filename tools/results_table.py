@@ -8,7 +8,7 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-CONFIGS = ["water3k", "rnase24k", "mem82k", "stmv", "stmv_fsw", "stmv_tab", "water12m"]
+CONFIGS = ["water3k", "rnase24k", "rnase24k_lb", "mem82k", "stmv", "stmv_fsw", "stmv_tab", "grappa1.5m", "water12m"]
 
 
 def main():
