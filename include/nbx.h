@@ -303,6 +303,11 @@ NBX_API int nbx_pme_set_box(nbx_pme* pme, const float box[3]);
  * reciprocal energy / virial into the context (read with nbx_pme_energy).                */
 NBX_API int nbx_pme_compute(nbx_pme* pme, int32_t n, const float* x_dev, const float* q_dev, float* f_dev,
                             uint32_t flags, void* stream);
+/* The same on the atoms of nonbonded context `ctx`'s grid `grid` (after nbx_put_x or the
+ * search step of that step), in its cluster order -- spatially sorted, so the spread and
+ * gather touch the charge grid with L2 locality -- with the forces added to the grid's
+ * cluster force buffer: the next nbx_get_f returns nonbonded + reciprocal forces.       */
+NBX_API int nbx_pme_compute_grid(nbx_pme* pme, nbx_ctx* ctx, int grid, uint32_t flags, void* stream);
 /* Reads and clears the accumulated energy and virial (row-major 3x3); syncs `stream`.   */
 NBX_API int nbx_pme_energy(nbx_pme* pme, double* e_host, double* virial_host, void* stream);
 NBX_API int64_t nbx_pme_launch_count(nbx_pme* pme);

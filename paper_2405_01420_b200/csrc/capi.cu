@@ -812,6 +812,18 @@ NBX_API int nbx_pme_compute(nbx_pme* pme, int32_t n, const float* x, const float
     NBX_GUARD_END
 }
 
+NBX_API int nbx_pme_compute_grid(nbx_pme* pme, nbx_ctx* ctx, int grid, uint32_t flags, void* stream)
+{
+    NBX_GUARD_BEGIN
+    NBX_CHECK_CTX(pme);
+    if (!ctx || ctx->device != pme->device) return fail(NBX_EINVAL, "PME and nonbonded contexts on different devices");
+    if (grid < 0 || grid > 1) return fail(NBX_EINVAL, "bad grid index");
+    if (!pme->have_box) return fail(NBX_EINVAL, "PME compute before set_box");
+    pme_compute_grid(pme, ctx, grid, flags, (cudaStream_t)stream);
+    return NBX_OK;
+    NBX_GUARD_END
+}
+
 NBX_API int nbx_pme_energy(nbx_pme* pme, double* e_host, double* virial_host, void* stream)
 {
     NBX_GUARD_BEGIN

@@ -219,7 +219,8 @@ ForceConsts make_force_consts(const nbx_consts& c);
 void pme_setup(nbx_pme* pme);
 void pme_set_box(nbx_pme* pme, const float box[3]);
 void pme_compute(nbx_pme* pme, int n, const float* x, const float* q, float* f, unsigned flags, cudaStream_t st,
-                 cudaEvent_t* ev = nullptr);
+                 cudaEvent_t* ev = nullptr, bool xq4 = false);
+void pme_compute_grid(nbx_pme* pme, nbx_ctx* ctx, int grid, unsigned flags, cudaStream_t st);
 void pme_profile(nbx_pme* pme, int n, const float* x, const float* q, float* f, float ms[6], cudaStream_t st);
 void pme_energy(nbx_pme* pme, double* e, double* vir, cudaStream_t st);
 void pme_release(nbx_pme* pme);

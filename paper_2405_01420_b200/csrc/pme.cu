@@ -70,8 +70,29 @@ __device__ __forceinline__ float sel4(const float v[4], int j)
     return j == 0 ? v[0] : (j == 1 ? v[1] : (j == 2 ? v[2] : v[3]));
 }
 
+// atom a's position and charge: [n][3] + [n] arrays, or (XQ4) the nonbonded grid's
+// cluster-ordered float4 (x, y, z, q) buffer (fillers have q = 0 and are skipped)
+template <bool XQ4>
+__device__ __forceinline__ void load_atom(int a, const float* __restrict__ x, const float* __restrict__ q, float& px,
+                                          float& py, float& pz, float& qa)
+{
+    if (XQ4) {
+        const float4 t = reinterpret_cast<const float4*>(x)[a];
+        px = t.x;
+        py = t.y;
+        pz = t.z;
+        qa = t.w;
+    } else {
+        px = x[3 * a + 0];
+        py = x[3 * a + 1];
+        pz = x[3 * a + 2];
+        qa = q[a];
+    }
+}
+
 // 4 threads per atom (one z spline point each, 16 (x, y) points in a loop): 4 adjacent threads
 // add into 4 consecutive z points, and the B-spline weights are computed 4x per atom, not 16x
+template <bool XQ4>
 __global__ void __launch_bounds__(PME_THREADS) k_pme_spread(int n, const float* __restrict__ x,
                                                             const float* __restrict__ q, PmeGeom g,
                                                             float* __restrict__ grid)
@@ -79,13 +100,14 @@ __global__ void __launch_bounds__(PME_THREADS) k_pme_spread(int n, const float* 
     const int a = (blockIdx.x * PME_THREADS + threadIdx.x) >> 2;
     const int jz = threadIdx.x & 3;
     if (a >= n) return;
-    const float qa = q[a];
+    float px, py, pz, qa;
+    load_atom<XQ4>(a, x, q, px, py, pz, qa);
     if (qa == 0.0f) return;
     int ix, iy, iz;
     float wx, wy, wz, tx[4], ty[4], tz[4], d[4];
-    frac_index(x[3 * a + 0], g.ibx, g.nx, ix, wx);
-    frac_index(x[3 * a + 1], g.iby, g.ny, iy, wy);
-    frac_index(x[3 * a + 2], g.ibz, g.nz, iz, wz);
+    frac_index(px, g.ibx, g.nx, ix, wx);
+    frac_index(py, g.iby, g.ny, iy, wy);
+    frac_index(pz, g.ibz, g.nz, iz, wz);
     bspline4(wx, tx, d);
     bspline4(wy, ty, d);
     bspline4(wz, tz, d);
@@ -159,6 +181,9 @@ __global__ void __launch_bounds__(256) k_pme_solve(PmeGeom g, float beta, float 
 }
 
 // 4 threads per atom (one z spline point each, 16 (x, y) points), 2 xor shuffles
+// XQ4: forces are added to the nonbonded grid's cluster force buffer (float4 per slot), which
+// the F buffer op then returns in the caller's atom order together with the nonbonded forces
+template <bool XQ4>
 __global__ void __launch_bounds__(PME_THREADS) k_pme_gather(int n, const float* __restrict__ x,
                                                             const float* __restrict__ q, PmeGeom g, float epsfac,
                                                             const float* __restrict__ phi, float* __restrict__ f)
@@ -167,12 +192,13 @@ __global__ void __launch_bounds__(PME_THREADS) k_pme_gather(int n, const float* 
     const int jz = threadIdx.x & 3;
     const bool live = a < n;
     const int ac = live ? a : n - 1;
-    const float qa = q[ac];
+    float px, py, pz, qa;
+    load_atom<XQ4>(ac, x, q, px, py, pz, qa);
     int ix, iy, iz;
     float wx, wy, wz, tx[4], ty[4], tz[4], dx[4], dy[4], dz[4];
-    frac_index(x[3 * ac + 0], g.ibx, g.nx, ix, wx);
-    frac_index(x[3 * ac + 1], g.iby, g.ny, iy, wy);
-    frac_index(x[3 * ac + 2], g.ibz, g.nz, iz, wz);
+    frac_index(px, g.ibx, g.nx, ix, wx);
+    frac_index(py, g.iby, g.ny, iy, wy);
+    frac_index(pz, g.ibz, g.nz, iz, wz);
     bspline4(wx, tx, dx);
     bspline4(wy, ty, dy);
     bspline4(wz, tz, dz);
@@ -205,9 +231,10 @@ __global__ void __launch_bounds__(PME_THREADS) k_pme_gather(int n, const float* 
     }
     if (live && jz == 0 && qa != 0.0f) {
         const float s = -epsfac * qa;
-        f[3 * a + 0] += s * (float)g.nx * g.ibx * sx;
-        f[3 * a + 1] += s * (float)g.ny * g.iby * sy;
-        f[3 * a + 2] += s * (float)g.nz * g.ibz * sz;
+        float* fa = f + (XQ4 ? 4 : 3) * a;
+        fa[0] += s * (float)g.nx * g.ibx * sx;
+        fa[1] += s * (float)g.ny * g.iby * sy;
+        fa[2] += s * (float)g.nz * g.ibz * sz;
     }
 }
 
@@ -291,7 +318,7 @@ static PmeGeom geom(const nbx_pme* pme)
 // ev (optional, 7 events): recorded before the memset and after each of the 6 stages
 // (memset, spread, R2C, solve, C2R, gather) -- nbx_pme_profile's per-stage times
 void pme_compute(nbx_pme* pme, int n, const float* x, const float* q, float* f, unsigned flags, cudaStream_t st,
-                 cudaEvent_t* ev)
+                 cudaEvent_t* ev, bool xq4)
 {
     const PmeGeom g = geom(pme);
     const size_t ng = (size_t)g.nx * g.ny * g.nz;
@@ -299,7 +326,10 @@ void pme_compute(nbx_pme* pme, int n, const float* x, const float* q, float* f, 
     NBX_CUDA(cudaMemsetAsync(pme->grid.p, 0, sizeof(float) * ng, st)); // GRID_MEMSET
     if (ev) NBX_CUDA(cudaEventRecord(ev[1], st));
     const int blocks = (int)(((long long)n * 4 + PME_THREADS - 1) / PME_THREADS);
-    if (n > 0) k_pme_spread<<<blocks, PME_THREADS, 0, st>>>(n, x, q, g, pme->grid.p);
+    if (n > 0) {
+        if (xq4) k_pme_spread<true><<<blocks, PME_THREADS, 0, st>>>(n, x, q, g, pme->grid.p);
+        else k_pme_spread<false><<<blocks, PME_THREADS, 0, st>>>(n, x, q, g, pme->grid.p);
+    }
     NBX_CUDA(cudaGetLastError());
     if (ev) NBX_CUDA(cudaEventRecord(ev[2], st));
     if (cufftSetStream(pme->fwd, st) != CUFFT_SUCCESS || cufftSetStream(pme->inv, st) != CUFFT_SUCCESS)
@@ -317,7 +347,10 @@ void pme_compute(nbx_pme* pme, int n, const float* x, const float* q, float* f, 
     if (cufftExecC2R(pme->inv, reinterpret_cast<cufftComplex*>(pme->spec.p), pme->grid.p) != CUFFT_SUCCESS)
         throw CudaError{cudaErrorLaunchFailure, "cufftExecC2R"};
     if (ev) NBX_CUDA(cudaEventRecord(ev[5], st));
-    if (n > 0) k_pme_gather<<<blocks, PME_THREADS, 0, st>>>(n, x, q, g, pme->epsfac, pme->grid.p, f);
+    if (n > 0) {
+        if (xq4) k_pme_gather<true><<<blocks, PME_THREADS, 0, st>>>(n, x, q, g, pme->epsfac, pme->grid.p, f);
+        else k_pme_gather<false><<<blocks, PME_THREADS, 0, st>>>(n, x, q, g, pme->epsfac, pme->grid.p, f);
+    }
     NBX_CUDA(cudaGetLastError());
     if (ev) NBX_CUDA(cudaEventRecord(ev[6], st));
     pme->launches += (n > 0 ? 3 : 1);
@@ -331,6 +364,16 @@ void pme_profile(nbx_pme* pme, int n, const float* x, const float* q, float* f, 
     NBX_CUDA(cudaEventSynchronize(ev[6]));
     for (int k = 0; k < 6; k++) NBX_CUDA(cudaEventElapsedTime(&ms[k], ev[k], ev[k + 1]));
     for (int k = 0; k < 7; k++) cudaEventDestroy(ev[k]);
+}
+
+// PME on the atoms of a nonbonded context's grid, in its cluster order (spatially sorted:
+// neighbouring atoms touch neighbouring grid points), forces into its cluster force buffer
+void pme_compute_grid(nbx_pme* pme, nbx_ctx* ctx, int g, unsigned flags, cudaStream_t st)
+{
+    Grid& G = ctx->grid[g];
+    if (!G.built) throw CudaError{cudaErrorInvalidValue, "PME on a grid before grid build"};
+    pme_compute(pme, G.nslots, reinterpret_cast<const float*>(G.xq.p), nullptr, reinterpret_cast<float*>(G.f.p),
+                flags, st, nullptr, true);
 }
 
 void pme_energy(nbx_pme* pme, double* e, double* vir, cudaStream_t st)

@@ -70,7 +70,7 @@ EXPORTS = ["nbx_last_error", "nbx_version", "nbx_derive_consts", "nbx_ewald_tabl
            "nbx_peer_init", "nbx_peer_open", "nbx_peer_set_halo", "nbx_peer_put_x", "nbx_peer_halo_x",
            "nbx_peer_force_nonlocal", "nbx_peer_get_f", "nbx_peer_status",
            "nbx_pme_create", "nbx_pme_destroy", "nbx_pme_set_box", "nbx_pme_compute", "nbx_pme_energy",
-           "nbx_pme_launch_count", "nbx_pme_profile", "nbx_leapfrog"]
+           "nbx_pme_launch_count", "nbx_pme_profile", "nbx_pme_compute_grid", "nbx_leapfrog"]
 
 _lib = None
 
@@ -127,6 +127,7 @@ def lib():
         L.nbx_pme_launch_count.argtypes = [vp]
         L.nbx_pme_launch_count.restype = C.c_int64
         L.nbx_pme_profile.argtypes = [vp, i32, vp, vp, vp, vp, vp]
+        L.nbx_pme_compute_grid.argtypes = [vp, vp, C.c_int, u32, vp]
         L.nbx_leapfrog.argtypes = [i32, vp, vp, vp, vp, C.c_float, vp]
         _lib = L
     return _lib
@@ -281,12 +282,14 @@ class Nonbonded:
         check(lib().nbx_step_graph(self.ctx.h, _dev_ptr(x), _dev_ptr(f), 1 if prune else 0,
                                    _stream(self.torch, stream)))
 
-    def step(self, x, f, step, energy=False, virial=False, stream=None, graphs=False):
+    def step(self, x, f, step, energy=False, virial=False, stream=None, graphs=False, pme=None):
         """One NB-path MD step with the reference cadence (pipeline.py:222-235).
-        graphs=True replays non-search, non-energy steps as a captured CUDA graph."""
+        graphs=True replays non-search, non-energy steps as a captured CUDA graph.
+        pme (paper_2405_01420_b200.pme.Pme): add the reciprocal-space forces on the grid's
+        cluster-ordered atoms before the F buffer op (f = nonbonded + PME)."""
         search = step % self.nstlist == 0
         prune = (not search) and self.prune_every and step % self.prune_every == 0
-        if graphs and not search and not (energy or virial):
+        if graphs and pme is None and not search and not (energy or virial):
             self.graph_step(x, f, prune=bool(prune), stream=stream)
             return None
         if search:
@@ -297,6 +300,8 @@ class Nonbonded:
                 self.prune(stream=stream)
         self.compute(energy=energy, virial=virial, stream=stream)
         res = self.energies(stream) if (energy or virial) else None
+        if pme is not None:
+            pme.compute_grid(self, energy=energy, virial=virial, stream=stream)
         self.get_f(f, stream=stream)
         return res
 

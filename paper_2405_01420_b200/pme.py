@@ -90,6 +90,24 @@ class Pme:
                                            C.c_void_p(st)))
         return f, (float(e[0]), v.reshape(3, 3))
 
+    def compute_grid(self, nb, energy=False, virial=False, grid=0, stream=None):
+        """Reciprocal-space forces on the atoms of Nonbonded `nb`'s grid (cluster order, after
+        its X op of this step), added to its cluster force buffer: nb.get_f() then returns
+        nonbonded + PME forces.  Energy / virial accumulate here (read with energy())."""
+        import torch
+        st = torch.cuda.current_stream().cuda_stream if stream is None else stream
+        flags = (1 if energy else 0) | (2 if virial else 0)
+        nbx.check(nbx.lib().nbx_pme_compute_grid(self.h, nb.ctx.h, grid, flags, C.c_void_p(st)))
+
+    def energy(self, stream=None):
+        import torch
+        st = torch.cuda.current_stream().cuda_stream if stream is None else stream
+        e = np.zeros(1)
+        v = np.zeros(9)
+        nbx.check(nbx.lib().nbx_pme_energy(self.h, e.ctypes.data_as(C.c_void_p), v.ctypes.data_as(C.c_void_p),
+                                           C.c_void_p(st)))
+        return float(e[0]), v.reshape(3, 3)
+
     STAGES = ("grid_memset", "pme_spread", "fft_3d_forward", "pme_solve", "fft_3d_inverse", "pme_gather")
 
     def profile(self, x, q, out=None):

@@ -103,3 +103,32 @@ def test_pme_profile_stages(gpu):
     f2 = pm.compute(x, q)
     torch.cuda.synchronize()
     assert float((f - f2).norm() / f2.norm()) < 1e-5
+
+
+@pytest.mark.parametrize("config", ["rnase24k", "water12m"])
+def test_pme_on_nonbonded_grid(gpu, config):
+    """nbx_pme_compute_grid: PME on the nonbonded grid's cluster-ordered atoms with the forces
+    added to its cluster force buffer -- Nonbonded.step(pme=...) returns NB + PME forces equal
+    to the NB step plus the user-order PME (fp32 atomics: rel 1e-5)."""
+    import torch
+    from paper_2405_01420_b200 import nbx, pme
+    s = systems.make(config, 30000 if config == "water12m" else None)
+    nb = nbx.Nonbonded(s)
+    pm = pme.Pme.for_system(s)
+    x, q = _dev(s.x), _dev(s.q)
+    f1 = torch.empty_like(x)
+    f2 = torch.empty_like(x)
+    for k in range(3):
+        nb.step(x, f1, k, pme=pm)
+    nb.step(x, f2, 3)
+    f2p = pm.compute(x, q, out=f2.clone())
+    f1b = torch.empty_like(x)
+    nb.step(x, f1b, 4, pme=pm)
+    e_grid = None
+    nb.step(x, f1b, 5, energy=True, pme=pm)
+    e_grid, _ = pm.energy()
+    _, (e_user, _) = pm.compute(x, q, energy=True)
+    torch.cuda.synchronize()
+    rel = float((f1b - f2p).norm() / f2p.norm())
+    assert rel < 1e-5, rel
+    assert abs(e_grid - e_user) <= 1e-5 * abs(e_user)
