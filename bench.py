@@ -151,7 +151,7 @@ def cpu_sample_system(config):
     """A bounded sample of the workload for the CPU port: same generator/parameters, fewer atoms."""
     from paper_2405_01420_b200 import systems
     n = {"water3k": None, "rnase24k": None, "mem82k": 24000, "stmv": 48000, "stmv_fsw": 48000, "stmv_tab": 48000,
-         "water12m": 48000}[config]
+         "water12m": 48000, "rnase24k_lb": None, "rnase24k_geom": None, "grappa1.5m": 48000}[config]
     return systems.make(config, n), n
 
 
