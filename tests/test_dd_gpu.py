@@ -48,3 +48,28 @@ def test_dd_matches_single_gpu(gpu, world, halo):
     assert_forces(d["fa"], d["f_ref"])
     assert_forces(d["fb"], d["f2_ref"])
     assert_forces(d["fb2"], d["f2_ref"])
+
+
+@pytest.mark.parametrize("config", ["stmv_tab", "grappa1.5m", "rnase24k_lb"])
+@pytest.mark.parametrize("world", [2, 4])
+def test_dd_paper_flavours(gpu, world, config):
+    """The paper's kernel flavours through the DD path (NVLink peer halo): tabulated Ewald +
+    force-switch LJ (STMV flavour), tabulated Ewald + LB combination rule (Grappa flavour), and
+    LB on the protein-like box; forces, energies and virial == the single-GPU engine."""
+    if _ngpu() < world:
+        pytest.skip(f"needs {world} GPUs")
+    natoms = 60000 if config == "rnase24k_lb" else 150000
+    with tempfile.TemporaryDirectory() as tmp:
+        out = os.path.join(tmp, "dd.npz")
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+               "--master-addr", "127.0.0.1", "--master-port", str(29520 + world),
+               os.path.join(ROOT, "tests", "dd_gpu_worker.py"), config, str(natoms), out, "p2p"]
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+        assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+        d = np.load(out)
+    assert np.array_equal(np.sort(d["gids"]), np.arange(int(d["natoms"])))
+    assert_forces(d["f"], d["f_ref"])
+    assert_energies(d["e"], d["e_ref"])
+    assert_virial(d["vir"], d["vir_ref"])
+    assert_forces(d["fa"], d["f_ref"])
+    assert_forces(d["fb"], d["f2_ref"])
