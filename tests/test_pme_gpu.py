@@ -132,3 +132,23 @@ def test_pme_on_nonbonded_grid(gpu, config):
     rel = float((f1b - f2p).norm() / f2p.norm())
     assert rel < 1e-5, rel
     assert abs(e_grid - e_user) <= 1e-5 * abs(e_user)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_pme_random_noncubic_boxes(gpu, seed):
+    """Random rectangular boxes (edges 2.6-6 nm, uneven grid sizes), uniform random atoms
+    (some outside the box), random charges: GPU == oracle on the same grid."""
+    from paper_2405_01420_b200 import pme
+    rng = np.random.default_rng(100 + seed)
+    box = rng.uniform(2.6, 6.0, 3).astype(np.float32)
+    n = int(rng.integers(500, 5000))
+    x = (rng.uniform(-0.5, 1.5, (n, 3)) * box).astype(np.float32)
+    q = rng.uniform(-1, 1, n).astype(np.float32)
+    beta = float(rng.uniform(2.5, 3.5))
+    pm = pme.Pme(box, beta)
+    f, (e, vir) = pm.compute(_dev(x), _dev(q), energy=True, virial=True)
+    Eo, fo, vo = P.pme(x, q, box, beta, 138.935458, pm.nk, 4)
+    fg = f.cpu().numpy().astype(np.float64)
+    assert np.sqrt(((fg - fo) ** 2).sum() / (fo**2).sum()) <= FTOL
+    assert abs(e - Eo) / abs(Eo) <= ETOL
+    assert np.abs(vir - vo).max() / np.abs(vo).max() <= ETOL
