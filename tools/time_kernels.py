@@ -36,6 +36,7 @@ def main(cfg):
     r["prune_ms"] = timed(lambda: nb.prune(), 10)
     r["put_x_ms"] = timed(lambda: nb.put_x(x), 20)
     r["force_ms"] = timed(lambda: nb.compute(), 10)
+    r["force_virial_ms"] = timed(lambda: nb.compute(virial=True), 5)
     r["force_energy_ms"] = timed(lambda: nb.compute(energy=True, virial=True), 5)
     r["get_f_ms"] = timed(lambda: nb.get_f(f), 20)
     p, sl = nb.count_pairs()
