@@ -17,6 +17,7 @@ all host threads, rank 0 only) on a bounded sample of the same workload.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import subprocess
@@ -73,16 +74,20 @@ class ClockSampler:
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index=0):
+    def __init__(self, index=0, interval_ms=100, enabled=True):
         self.index = index
+        self.interval_ms = int(interval_ms)
+        self.enabled = enabled
         self.proc = None
         self.f = None
 
     def start(self):
+        if not self.enabled:
+            return self
         try:
             self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                          "-i", str(self.index), "-lms", "100"], stdout=self.f,
+                                          "-i", str(self.index), "-lms", str(self.interval_ms)], stdout=self.f,
                                          stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -220,7 +225,7 @@ def run_single(args):
     K = args.steps
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     evf = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
-    clocks = ClockSampler(0).start()
+    clocks = ClockSampler(0, interval_ms=250).start()  # NVML polls contend with CUDA calls
     torch.cuda.synchronize()
     l0 = nb.launch_count()
     n_search = n_prune = 0
@@ -355,6 +360,10 @@ def run_reference(args):
 
 def main():
     args = parse()
+    # no cyclic-GC pauses inside timed regions (a gen-2 pass during a Python-side search /
+    # repartition step stalls the GPU that step waits on); reference counting still frees
+    gc.collect()
+    gc.disable()
     if args.impl == "reference":
         run_reference(args)
         return

@@ -235,6 +235,9 @@ class DomainDecomposition:
         self._t_last = 0.0
         self.profile_phases = False  # record per-phase CUDA events in step() (bench breakdown)
         self.phase_log = []
+        # p2p steps: halo gather + nonlocal force on a side stream (NBX_DD_OVERLAP=0 disables)
+        self.overlap_nonlocal = os.environ.get("NBX_DD_OVERLAP", "1") != "0"
+        self._side = None
 
     # ---------------------------------------------------------------------- partitioning
     def _exchange(self, sends, recvs):
@@ -483,6 +486,31 @@ class DomainDecomposition:
         if ev:
             ev[0].record()
         eng.peer_put_x(x, seq)  # grid-0 X op + publish + signal
+        if self.overlap_nonlocal and not ev:
+            # halo gather + nonlocal force on a side stream: they start as soon as the owners
+            # have published and overlap the local kernel's tail (the two lists use separate
+            # work counters; both red.add into the home cluster forces)
+            torch = self.torch
+            main = torch.cuda.current_stream()
+            if self._side is None:
+                self._side = torch.cuda.Stream(device=self.device)
+                self._ev_x = torch.cuda.Event()
+                self._ev_nl = torch.cuda.Event()
+            self._ev_x.record(main)
+            with torch.cuda.stream(self._side):
+                self._side.wait_event(self._ev_x)
+                eng.peer_halo_x(seq)
+                if prune:
+                    eng.prune(1)
+                eng.peer_force_nonlocal(seq)
+                self._ev_nl.record(self._side)
+            if prune:
+                eng.prune(0)
+            eng.force(0, 0)
+            main.wait_event(self._ev_nl)
+            f_home = self.f_ext[:self.n_home]
+            eng.peer_get_f(f_home, seq)  # wait for the senders, home forces + inbox
+            return f_home
         if prune:
             eng.prune(0)
         eng.force(0, 0)
@@ -557,7 +585,9 @@ def bench(args, METRIC, UNIT, FLOPS_PER_PAIR, DESC, ClockSampler, time_cpu_port,
 
     K = args.steps
     st = torch.cuda.current_stream()
-    clocks = ClockSampler(local).start()
+    # clocks sampled by rank 0 only, every 250 ms: each nvidia-smi poll takes NVML locks that a
+    # rank's CUDA calls can wait on, and search steps synchronise with the host
+    clocks = ClockSampler(local, interval_ms=250, enabled=(rank == 0)).start()
     dist.barrier()
     torch.cuda.synchronize()
     l0 = dd.engine.launch_count()
