@@ -96,3 +96,24 @@ def test_halo_entry_points_validate_arguments():
     assert lib.nbx_halo_pack_x(None, None, -1, None, None, None) == 1
     assert lib.nbx_halo_unpack_add_f(None, None, 5, None, None) == 1
     assert lib.nbx_halo_pack_x(None, None, 0, None, None, None) == 0
+
+
+def test_pme_no_cpu_fallback_and_validation():
+    """Row f4 entry points: parameter validation happens before device checks, and without a
+    usable sm_100 GPU a PME context fails with NBX_ECUDA; the leap-frog validates arguments."""
+    import torch
+
+    from paper_2405_01420_b200 import pme
+    with pytest.raises(nbx.NbxError) as ei:
+        pme.Pme([3.0, 3.0, 3.0], 3.0, nk=(25, 24, 24))
+    assert ei.value.code == 1
+    with pytest.raises(nbx.NbxError):
+        pme.Pme([3.0, 3.0, 3.0], 3.0, order=6)
+    if not torch.cuda.is_available():
+        with pytest.raises(nbx.NbxError) as ei:
+            pme.Pme([3.0, 3.0, 3.0], 3.0)
+        assert ei.value.code == 2 and "no CPU fallback" in str(ei.value)
+    lib = nbx.lib()
+    assert lib.nbx_leapfrog(-1, None, None, None, None, 0.0, None) == 1
+    assert lib.nbx_leapfrog(0, None, None, None, None, 0.0, None) == 0
+    assert lib.nbx_pme_compute(None, 0, None, None, None, 0, None) == 1
