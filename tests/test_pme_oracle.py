@@ -111,3 +111,15 @@ def test_full_ewald_energy():
     # the fp32 real-space pair energies cancel (E_coul within 5e-5 of
     # exact), so the bar is relative to the size of the two halves, not to their sum
     assert abs((e[1] + Erec) - E_ref) < 5e-5 * (abs(Ereal) + abs(Erec_d))
+
+
+def test_pme_oracle_matches_golden_direct_sum():
+    """tests/golden/ewald_recip_600.npz (tools/make_golden.py): the exact reciprocal-space sum
+    of a random neutral box; the oracle PME at order 6 / 0.05 nm reproduces it."""
+    import os
+    d = np.load(os.path.join(os.path.dirname(__file__), "golden", "ewald_recip_600.npz"))
+    x, q, box, beta, eps = d["x"], d["q"], d["box"], float(d["beta"]), float(d["epsfac"])
+    E, f, v = P.pme(x, q, box, beta, eps, P.grid_dims(box, 0.05, 6), 6)
+    assert abs(E - float(d["energy"])) / abs(float(d["energy"])) < 2e-6
+    assert np.sqrt(((f - d["f"]) ** 2).sum() / (d["f"] ** 2).sum()) < 1e-5
+    assert np.abs(v - d["virial"]).max() / np.abs(d["virial"]).max() < 1e-5

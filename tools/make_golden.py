@@ -2,6 +2,7 @@
 
 brute_*.npz   small synthetic systems with float64 brute-force forces/energies/virial
               (oracle/brute.py, exact erfc) plus the oracle's list sizes and list CRC.
+ewald_recip_600.npz  exact reciprocal Ewald sum of a random neutral box (PME anchor, row f4).
 costs_golden.json  the reference simulator's own cost-law outputs (imported from
               /root/reference/pkg/src, run in THIS container only) for the adapter tests.
 """
@@ -38,6 +39,23 @@ def brute_fixture(tag, s, coul_tol):
     print(tag, s.natoms, sz)
 
 
+def ewald_recip_fixture():
+    """Row f4: exact reciprocal-space Ewald sum (float64, explicit k vectors) of a random
+    neutral 600-atom box, the anchor for the PME oracle and the GPU PME."""
+    from oracle import pme as P
+    rng = np.random.default_rng(2024)
+    box = np.array([2.8, 3.1, 2.9])
+    n = 600
+    x = rng.uniform(0, 1, (n, 3)) * box
+    q = rng.uniform(-1, 1, n)
+    q -= q.mean()
+    beta, eps = 3.1234, 138.935458
+    E, f, v = P.ewald_recip_direct(x, q, box, beta, eps, tol=1e-14)
+    np.savez_compressed(os.path.join(OUT, "ewald_recip_600.npz"), x=x, q=q, box=box, beta=beta, epsfac=eps,
+                        energy=E, f=f, virial=v)
+    print("ewald_recip_600", E)
+
+
 def costs_golden():
     sys.path.insert(0, "/root/reference/pkg/src")
     from mdgpusim import costs, presets  # noqa
@@ -56,11 +74,16 @@ def costs_golden():
     print("costs_golden.json", len(out["points"]))
 
 
+if __name__ == "__main__" and "--ewald-only" in sys.argv:
+    ewald_recip_fixture()
+    sys.exit(0)
+
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
     brute_fixture("water_rf_1500", systems.water_box(500, seed=11, coulomb="rf", rc=0.9, rlist_outer=1.0,
                                                      rlist_inner=0.92), 2e-6)
     brute_fixture("protein_ewald_3000", systems.protein_box(3000, seed=12, rc=1.0), 5e-5)
     brute_fixture("membrane_ewald_3000", systems.membrane_box(3000, seed=13, rc=1.0), 5e-5)
+    ewald_recip_fixture()
     if os.path.isdir("/root/reference/pkg/src"):
         costs_golden()
