@@ -298,11 +298,28 @@ class DomainDecomposition:
             p.up_peer = coords_rank(c, self.dims)
             lo_d, hi_d = lo[d], lo[d] + self.D[d]
             # half-shell import: down-going messages carry home and imported atoms near the
-            # lower face; up-going ones only imported atoms near the upper face (see header)
-            p.down_idx = torch.nonzero(X[:, d] < lo_d + self.rl).flatten().to(torch.int32)
-            up = (X[:, d] >= hi_d - self.rl)
-            up[:self.n_home] = False
-            p.up_idx = torch.nonzero(up).flatten().to(torch.int32)
+            # lower face; up-going ones only imported atoms near the upper face (see header).
+            # Both index sets come from one nonzero (one host sync); coordinates and the
+            # (gid, owner, home index) metadata travel as one packed float32 [n, 6] message
+            # per direction (the int32 metadata bit-cast), so a pulse is one count round trip
+            # and one data round trip.
+            down_m = X[:, d] < lo_d + self.rl
+            up_m = X[:, d] >= hi_d - self.rl
+            up_m[:self.n_home] = False
+            # counts on the device, exchanged while the index sets are extracted; one host read
+            # of all four counts after the single nonzero
+            cnt_send = torch.stack([down_m.sum(), up_m.sum()]).to(torch.int64)
+            cnt_from_up = torch.zeros(2, dtype=torch.int64, device=dev)
+            cnt_from_down = torch.zeros(2, dtype=torch.int64, device=dev)
+            works = self._exchange([(cnt_send, p.down_peer), (cnt_send, p.up_peer)],
+                                   [(cnt_from_up, p.up_peer), (cnt_from_down, p.down_peer)])
+            nz = torch.nonzero(torch.stack([down_m, up_m]))[:, 1].to(torch.int32)
+            for w in works:
+                w.wait()
+            n_down, _, p.n_from_up, p.n_from_down = (
+                int(v) for v in torch.stack([cnt_send[0], cnt_send[1], cnt_from_up[0], cnt_from_down[1]]).tolist())
+            p.down_idx = nz[:n_down]
+            p.up_idx = nz[n_down:]
             sd = np.zeros(3, np.float32)
             su = np.zeros(3, np.float32)
             if self.coord[d] == 0:
@@ -310,31 +327,21 @@ class DomainDecomposition:
             if self.coord[d] == n_d - 1:
                 su[d] = -self.box[d]
             p.shift_down, p.shift_up = sd, su
-            # sizes
-            cnt_send = torch.tensor([p.down_idx.numel(), p.up_idx.numel()], dtype=torch.int64, device=dev)
-            cnt_from_up = torch.zeros(2, dtype=torch.int64, device=dev)
-            cnt_from_down = torch.zeros(2, dtype=torch.int64, device=dev)
-            for w in self._exchange([(cnt_send, p.down_peer), (cnt_send, p.up_peer)],
-                                    [(cnt_from_up, p.up_peer), (cnt_from_down, p.down_peer)]):
-                w.wait()
-            p.n_from_up = int(cnt_from_up[0])  # the up neighbour's down set
-            p.n_from_down = int(cnt_from_down[1])  # the down neighbour's up set
             n0 = X.shape[0]
             p.off_from_up, p.off_from_down = n0, n0 + p.n_from_up
-            send_d = (X[p.down_idx.long()] + torch.from_numpy(sd).to(dev)).contiguous()
-            send_u = (X[p.up_idx.long()] + torch.from_numpy(su).to(dev)).contiguous()
-            recv_u = torch.empty((p.n_from_up, 3), dtype=torch.float32, device=dev)
-            recv_d = torch.empty((p.n_from_down, 3), dtype=torch.float32, device=dev)
-            gsd, gsu = M[p.down_idx.long()].contiguous(), M[p.up_idx.long()].contiguous()
-            gru = torch.empty((p.n_from_up, 3), dtype=torch.int32, device=dev)
-            grd = torch.empty((p.n_from_down, 3), dtype=torch.int32, device=dev)
-            for w in self._exchange([(send_d, p.down_peer), (send_u, p.up_peer), (gsd, p.down_peer),
-                                     (gsu, p.up_peer)],
-                                    [(recv_u, p.up_peer), (recv_d, p.down_peer), (gru, p.up_peer),
-                                     (grd, p.down_peer)]):
+            XM = torch.cat([X, M.view(torch.float32)], dim=1)  # [n, 6]: x, y, z | gid, owner, home
+            send_d = XM[p.down_idx.long()]
+            send_d[:, :3] += torch.from_numpy(sd).to(dev)
+            send_u = XM[p.up_idx.long()]
+            send_u[:, :3] += torch.from_numpy(su).to(dev)
+            recv_u = torch.empty((p.n_from_up, 6), dtype=torch.float32, device=dev)
+            recv_d = torch.empty((p.n_from_down, 6), dtype=torch.float32, device=dev)
+            for w in self._exchange([(send_d, p.down_peer), (send_u, p.up_peer)],
+                                    [(recv_u, p.up_peer), (recv_d, p.down_peer)]):
                 w.wait()
-            X = torch.cat([X, recv_u, recv_d])
-            M = torch.cat([M, gru, grd])
+            R = torch.cat([recv_u, recv_d])
+            X = torch.cat([X, R[:, :3]])
+            M = torch.cat([M, R[:, 3:].contiguous().view(torch.int32)])
             self.pulses.append(p)
             self._tick(f"pulse{d}")
         self.n_ext = X.shape[0]
