@@ -594,7 +594,8 @@ def bench(args, METRIC, UNIT, FLOPS_PER_PAIR, DESC, ClockSampler, time_cpu_port,
     st = torch.cuda.current_stream()
     # clocks sampled by rank 0 only, every 250 ms: each nvidia-smi poll takes NVML locks that a
     # rank's CUDA calls can wait on, and search steps synchronise with the host
-    clocks = ClockSampler(local, interval_ms=250, enabled=(rank == 0)).start()
+    clocks = ClockSampler(local, interval_ms=250,
+                          enabled=(rank == 0 and os.environ.get("NBX_BENCH_CLOCKS", "1") != "0")).start()
     dist.barrier()
     torch.cuda.synchronize()
     l0 = dd.engine.launch_count()
@@ -603,11 +604,14 @@ def bench(args, METRIC, UNIT, FLOPS_PER_PAIR, DESC, ClockSampler, time_cpu_port,
     e0.record(st)
     n_search = 0
     search_steps = []
+    rep_cpu_ms = []  # host time of each repartition call on this rank (diagnostics)
     for k in range(K):
         step = args.warmup + k
         evs[k].record(st)
         if step % s.nstlist == 0:
+            tc = time.perf_counter()
             dd.repartition(xg)  # atoms re-assigned from the global coordinates
+            rep_cpu_ms.append(1e3 * (time.perf_counter() - tc))
             n_search += 1
             search_steps.append(k)
             x_home = dd.x_ext[:dd.n_home].clone()
@@ -627,6 +631,10 @@ def bench(args, METRIC, UNIT, FLOPS_PER_PAIR, DESC, ClockSampler, time_cpu_port,
     clk = clocks.stop()
     step_ms = sorted(evs[k].elapsed_time(evs[k + 1]) for k in range(K))
     search_ms = [evs[k].elapsed_time(evs[k + 1]) for k in search_steps]
+    rc = torch.tensor(rep_cpu_ms or [0.0], dtype=torch.float64, device=dev)
+    rc_all = [torch.zeros_like(rc) for _ in range(world)]
+    dist.all_gather(rc_all, rc)
+    rep_cpu_all = [[round(float(v), 1) for v in r] for r in rc_all]
     # per-phase breakdown on 10 extra (untimed) steps, all ranks starting together
     dist.barrier()
     torch.cuda.synchronize()
@@ -685,6 +693,7 @@ def bench(args, METRIC, UNIT, FLOPS_PER_PAIR, DESC, ClockSampler, time_cpu_port,
             "e2e": e2e, "gpu_launches": int(launches), "clocks": clk, "searches": n_search,
             "dd_phases_ms_rank0": phases,
             "step_ms_rank0": {"median": step_ms[K // 2], "max": step_ms[-1], "search_steps": search_ms},
+            "repartition_host_ms_per_rank": rep_cpu_all,
         }
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
