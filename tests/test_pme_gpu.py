@@ -167,3 +167,24 @@ def test_gpu_pme_against_golden_direct_sum(gpu):
     assert abs(e - float(d["energy"])) / abs(float(d["energy"])) < 1e-4
     assert np.sqrt(((fg - d["f"]) ** 2).sum() / (d["f"] ** 2).sum()) < 5e-4
     assert np.abs(vir - d["virial"]).max() / np.abs(d["virial"]).max() < 5e-4
+
+
+def test_pme_edge_cases(gpu):
+    """No atoms; all-zero charges; a bad grid index on the nonbonded-grid entry point."""
+    import torch
+    from paper_2405_01420_b200 import nbx, pme
+    pm = pme.Pme([3.0, 3.2, 3.4], 3.1)
+    x0 = torch.zeros((0, 3), device="cuda")
+    q0 = torch.zeros((0,), device="cuda")
+    f0, (e0, v0) = pm.compute(x0, q0, energy=True, virial=True)
+    assert f0.shape == (0, 3) and e0 == 0.0 and np.all(v0 == 0.0)
+    rng = np.random.default_rng(5)
+    x = _dev(rng.uniform(0, 3, (100, 3)))
+    fz, (ez, _) = pm.compute(x, torch.zeros(100, device="cuda"), energy=True)
+    torch.cuda.synchronize()
+    assert float(fz.abs().max()) == 0.0 and ez == 0.0
+    s = systems.make("rnase24k", 3000)
+    nb = nbx.Nonbonded(s)
+    nb.search(_dev(s.x))
+    with pytest.raises(nbx.NbxError):
+        nbx.check(nbx.lib().nbx_pme_compute_grid(pm.h, nb.ctx.h, 5, 0, None))
