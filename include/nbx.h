@@ -317,6 +317,13 @@ NBX_API int64_t nbx_pme_launch_count(nbx_pme* pme);
 NBX_API int nbx_pme_profile(nbx_pme* pme, int32_t n, const float* x_dev, const float* q_dev, float* f_dev,
                             float* ms_host, void* stream);
 
+/* One non-search step of a GPU-resident Ewald run as one CUDA graph launch: nbx_put_x(0)
+ * [+ nbx_prune(LOCAL) with NBX_STEP_PRUNE] + nbx_force(LOCAL) + nbx_pme_compute_grid(0) +
+ * nbx_get_f(0) + nbx_leapfrog(x, v, f, inv_mass, dt) (x and v updated in place).  Captured
+ * on first use per buffer set / dt and refreshed after searches or box changes.          */
+NBX_API int nbx_step_graph_pme(nbx_ctx* ctx, nbx_pme* pme, float* x_dev, float* f_dev, float* v_dev,
+                               const float* inv_mass_dev, float dt, uint32_t what, void* stream);
+
 /* Leap-frog update (KernelKind.LEAP_FROG, costs.py:39, pipeline.py:249-251), no
  * constraints: v += f inv_mass dt; x += v dt (device arrays, [n][3] floats).            */
 NBX_API int nbx_leapfrog(int32_t n, float* x_dev, float* v_dev, const float* f_dev, const float* inv_mass_dev,

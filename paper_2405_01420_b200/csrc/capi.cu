@@ -237,6 +237,7 @@ NBX_API int nbx_destroy(nbx_ctx* ctx)
     ctx->c6c12s.release(); ctx->acc.release(); ctx->sumq2.release(); ctx->counter.release();
     ctx->ewtab.release();
     for (auto& g : ctx->graphs) cudaGraphExecDestroy(g.exec);
+    for (auto& g : ctx->full_graphs) cudaGraphExecDestroy(g.exec);
     peer_release(ctx);
     if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
     delete ctx;
@@ -476,6 +477,82 @@ NBX_API int nbx_step_graph(nbx_ctx* ctx, const float* x, float* f, uint32_t what
         }
         cudaGraphDestroy(graph);
         g->epoch = ctx->epoch;
+        g->kernels = kernels;
+    }
+    NBX_CUDA(cudaGraphLaunch(g->exec, (cudaStream_t)stream));
+    ctx->launches += g->kernels;
+    return NBX_OK;
+    NBX_GUARD_END
+}
+
+// One full GPU-resident non-search step as one graph launch: X op (+ prune) + force + PME on
+// grid 0 (forces into the cluster buffer) + F op + leap-frog update of x and v in place.
+// Captured like nbx_step_graph; refreshed after a search, a topology/box change or a PME box
+// change.  For small boxes, where the ~12 separate launches of the step dominate.
+NBX_API int nbx_step_graph_pme(nbx_ctx* ctx, nbx_pme* pme, float* x, float* f, float* v, const float* inv_mass,
+                               float dt, uint32_t what, void* stream)
+{
+    NBX_GUARD_BEGIN
+    NBX_CHECK_CTX(ctx);
+    if (!pme || pme->device != ctx->device) return fail(NBX_EINVAL, "PME context missing or on another device");
+    if (!pme->have_box) return fail(NBX_EINVAL, "PME box not set");
+    if (!ctx->list[0].built) return fail(NBX_EINVAL, "list not built");
+    if (!x || !f || !v || !inv_mass) return fail(NBX_EINVAL, "null buffer");
+    if (what & ~(uint32_t)NBX_STEP_PRUNE) return fail(NBX_EINVAL, "unknown step flags");
+    nbx_ctx::FullGraph* g = nullptr;
+    for (auto& e : ctx->full_graphs)
+        if (e.pme == pme && e.x == x && e.f == f && e.v == v && e.inv_mass == inv_mass && e.dt == dt &&
+            e.what == what)
+            g = &e;
+    if (!g || g->epoch != ctx->epoch || g->pme_epoch != pme->epoch) {
+        if (!ctx->cap_stream)
+            NBX_CUDA(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+        cudaStream_t cs = ctx->cap_stream;
+        const int64_t l0 = ctx->launches, p0 = pme->launches;
+        const int n = ctx->grid[0].n;
+        cudaGraph_t graph = nullptr;
+        NBX_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
+        try {
+            put_x(ctx, 0, x, cs);
+            if (what & NBX_STEP_PRUNE) prune(ctx, 0, 0, 1, cs);
+            force(ctx, 0, 0, cs);
+            pme_compute_grid(pme, ctx, 0, 0u, cs);
+            get_f(ctx, 0, f, 0, cs);
+            leapfrog(n, x, v, f, inv_mass, dt, cs);
+        } catch (...) {
+            cudaStreamEndCapture(cs, &graph);
+            if (graph) cudaGraphDestroy(graph);
+            ctx->launches = l0;
+            pme->launches = p0;
+            throw;
+        }
+        NBX_CUDA(cudaStreamEndCapture(cs, &graph));
+        const int kernels = (int)(ctx->launches - l0) + (int)(pme->launches - p0) + 1;
+        ctx->launches = l0;
+        pme->launches = p0;
+        bool updated = false;
+        if (g) {
+            cudaGraphExecUpdateResultInfo info;
+            updated = cudaGraphExecUpdate(g->exec, graph, &info) == cudaSuccess;
+            if (!updated) {
+                cudaGetLastError();
+                cudaGraphExecDestroy(g->exec);
+            }
+        } else {
+            ctx->full_graphs.push_back(nbx_ctx::FullGraph{pme, 0, x, f, v, inv_mass, dt, what, 0, 0, nullptr});
+            g = &ctx->full_graphs.back();
+        }
+        if (!updated) {
+            cudaError_t e = cudaGraphInstantiate(&g->exec, graph, 0);
+            if (e != cudaSuccess) {
+                cudaGraphDestroy(graph);
+                ctx->full_graphs.erase(ctx->full_graphs.begin() + (g - ctx->full_graphs.data()));
+                NBX_CUDA(e);
+            }
+        }
+        cudaGraphDestroy(graph);
+        g->epoch = ctx->epoch;
+        g->pme_epoch = pme->epoch;
         g->kernels = kernels;
     }
     NBX_CUDA(cudaGraphLaunch(g->exec, (cudaStream_t)stream));

@@ -142,6 +142,22 @@ struct nbx_ctx {
     nbx::Peer* peer = nullptr;
     uint64_t epoch = 1;
     std::vector<StepGraph> graphs;
+    // nbx_step_graph_pme: the same plus PME on grid 0 and the leap-frog update, keyed by all
+    // buffers, the PME context (and its epoch) and dt
+    struct FullGraph {
+        const void* pme;
+        uint64_t pme_epoch;
+        const float* x;
+        float* f;
+        float* v;
+        const float* inv_mass;
+        float dt;
+        uint32_t what;
+        uint64_t epoch;
+        int kernels;
+        cudaGraphExec_t exec;
+    };
+    std::vector<FullGraph> full_graphs;
     cudaStream_t cap_stream = nullptr;
 };
 
@@ -159,6 +175,7 @@ struct nbx_pme {
     nbx::DBuf<double> acc;    // [0] energy, [1..9] virial
     cufftHandle fwd = 0, inv = 0;
     int64_t launches = 0;
+    uint64_t epoch = 1; // bumped by set_box (graph refresh)
 };
 
 namespace nbx {

@@ -20,6 +20,7 @@
 //    per-dimension modulus and Gaussian tables, fp64 block reduction of the energy and virial
 //    (energy steps only);
 //  * no CPU fallback: the context refuses to exist without an sm_100 device (capi.cu).
+#include <atomic>
 #include <cmath>
 #include <vector>
 
@@ -286,6 +287,10 @@ void pme_set_box(nbx_pme* pme, const float box[3])
 {
     for (int d = 0; d < 3; d++) pme->box[d] = box[d];
     pme->have_box = true;
+    // process-wide counter: a PME context created later at a freed one's address never
+    // matches a graph captured against the old one
+    static std::atomic<uint64_t> box_epoch{1};
+    pme->epoch = ++box_epoch;
     // per-dimension Gaussian factors exp(-pi^2 mt_d^2 / beta^2), mt_d = m_d / L_d (m_d signed)
     std::vector<float> t;
     const double pb = M_PI / (double)pme->beta;

@@ -70,7 +70,8 @@ EXPORTS = ["nbx_last_error", "nbx_version", "nbx_derive_consts", "nbx_ewald_tabl
            "nbx_peer_init", "nbx_peer_open", "nbx_peer_set_halo", "nbx_peer_put_x", "nbx_peer_halo_x",
            "nbx_peer_force_nonlocal", "nbx_peer_get_f", "nbx_peer_status",
            "nbx_pme_create", "nbx_pme_destroy", "nbx_pme_set_box", "nbx_pme_compute", "nbx_pme_energy",
-           "nbx_pme_launch_count", "nbx_pme_profile", "nbx_pme_compute_grid", "nbx_leapfrog"]
+           "nbx_pme_launch_count", "nbx_pme_profile", "nbx_pme_compute_grid", "nbx_leapfrog",
+           "nbx_step_graph_pme"]
 
 _lib = None
 
@@ -128,6 +129,7 @@ def lib():
         L.nbx_pme_launch_count.restype = C.c_int64
         L.nbx_pme_profile.argtypes = [vp, i32, vp, vp, vp, vp, vp]
         L.nbx_pme_compute_grid.argtypes = [vp, vp, C.c_int, u32, vp]
+        L.nbx_step_graph_pme.argtypes = [vp, vp, vp, vp, vp, vp, C.c_float, u32, vp]
         L.nbx_leapfrog.argtypes = [i32, vp, vp, vp, vp, C.c_float, vp]
         _lib = L
     return _lib
@@ -303,6 +305,26 @@ class Nonbonded:
         if pme is not None:
             pme.compute_grid(self, energy=energy, virial=virial, stream=stream)
         self.get_f(f, stream=stream)
+        return res
+
+    def md_step(self, x, f, v, inv_mass, dt, step, pme, energy=False, virial=False, stream=None, graphs=True):
+        """One GPU-resident MD step of a PME system: step() with pme (NB cadence + PME on the
+        grid's cluster order) followed by the leap-frog update of x and v in place
+        (pipeline.py:222-257, KernelKind.LEAP_FROG).  graphs=True replays non-search,
+        non-energy steps as ONE captured graph (nbx_step_graph_pme: X op, prune, force, PME
+        memset/spread/R2C/solve/C2R/gather, F op, update) -- launch overhead is what bounds
+        the small boxes."""
+        search = step % self.nstlist == 0
+        prune = (not search) and self.prune_every and step % self.prune_every == 0
+        if graphs and not search and not (energy or virial):
+            check(lib().nbx_step_graph_pme(self.ctx.h, pme.h, _dev_ptr(x), _dev_ptr(f), _dev_ptr(v),
+                                           _dev_ptr(inv_mass), C.c_float(dt), 1 if prune else 0,
+                                           _stream(self.torch, stream)))
+            return None
+        res = self.step(x, f, step, energy=energy, virial=virial, stream=stream, pme=pme)
+        st = _stream(self.torch, stream)
+        check(lib().nbx_leapfrog(int(x.shape[0]), _dev_ptr(x), _dev_ptr(v), _dev_ptr(f), _dev_ptr(inv_mass),
+                                 C.c_float(dt), st))
         return res
 
     # -- introspection -------------------------------------------------------------------

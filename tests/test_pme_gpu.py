@@ -188,3 +188,34 @@ def test_pme_edge_cases(gpu):
     nb.search(_dev(s.x))
     with pytest.raises(nbx.NbxError):
         nbx.check(nbx.lib().nbx_pme_compute_grid(pm.h, nb.ctx.h, 5, 0, None))
+
+
+def test_md_step_graph_matches_eager(gpu):
+    """nbx_step_graph_pme: a whole non-search MD step (X op, prune, force, PME, F op, leap-frog)
+    replayed as one graph gives the eager md_step's x and v, across searches (graph refreshed),
+    prune steps and a PME box reset (graph re-captured).  PME spreads with fp32 atomics, so the
+    two runs agree to rel 1e-5 in v, not bitwise."""
+    import dataclasses
+    import torch
+    from paper_2405_01420_b200 import nbx, pme
+    s = dataclasses.replace(systems.make("rnase24k"), nstlist=20, prune_every=5)
+    runs = []
+    for graphs in (False, True):
+        nb = nbx.Nonbonded(s)
+        pm = pme.Pme.for_system(s)
+        x = _dev(s.x)
+        v = torch.zeros_like(x)
+        f = torch.empty_like(x)
+        im = torch.full((s.natoms,), 0.1, dtype=torch.float32, device="cuda")
+        l0 = nb.launch_count()
+        for k in range(47):
+            if k == 33:
+                pm.set_box(s.box)
+            nb.md_step(x, f, v, im, 1e-4, k, pm, graphs=graphs)
+        torch.cuda.synchronize()
+        runs.append((x, v, nb.launch_count() - l0))
+    (xe, ve, _), (xg, vg, lg) = runs
+    assert float((vg - ve).norm() / ve.norm()) < 1e-5
+    assert float((xg - xe).abs().max()) < 1e-5
+    assert float(ve.norm()) > 0
+    assert lg >= 47 * 3  # graph replays count their kernel nodes

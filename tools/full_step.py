@@ -7,7 +7,9 @@ dt = 0 in the update: with no bonded forces or constraints the molecules would f
 positions are kept fixed; the update kernel still runs at full cost.  The result is an upper
 bound on the application rate (no listed forces, constraints or PME-PP communication).
 
-    python tools/full_step.py [config ...] [--steps K]
+    python tools/full_step.py [config ...] [--steps K] [--graphs]
+
+--graphs replays each non-search step as one CUDA graph (Nonbonded.md_step, nbx_step_graph_pme).
 """
 import json
 import os
@@ -19,7 +21,7 @@ import torch  # noqa: E402
 from paper_2405_01420_b200 import nbx, pme, systems  # noqa: E402
 
 
-def run(cfg, steps, grid_order=True):
+def run(cfg, steps, grid_order=True, graphs=False):
     s = systems.make(cfg)
     nb = nbx.Nonbonded(s)
     pm = pme.Pme.for_system(s)
@@ -31,6 +33,9 @@ def run(cfg, steps, grid_order=True):
     st = torch.cuda.current_stream()
 
     def one(k):
+        if graphs:  # non-search steps as one graph launch (nbx_step_graph_pme)
+            nb.md_step(x, f, v, im, 0.0, k, pm, graphs=True)
+            return
         if grid_order:  # PME on the NB grid's cluster-ordered atoms, forces via the F op
             nb.step(x, f, k, pme=pm)
         else:
@@ -48,7 +53,7 @@ def run(cfg, steps, grid_order=True):
     e1.record(st)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
-    out = {"config": cfg, "natoms": s.natoms, "steps": steps, "ms_per_step": ms, "pme_on_nb_grid": grid_order,
+    out = {"config": cfg, "natoms": s.natoms, "steps": steps, "ms_per_step": ms, "pme_on_nb_grid": grid_order, "graphs": graphs,
            "ns_per_day_upper_bound": 86.4 * s.dt_fs / ms if hasattr(s, "dt_fs") else 86.4 * 2.0 / ms,
            "pme_grid": pm.nk, "gpu_launches_nb_pme": nb.launch_count() + pm.launch_count()}
     print(json.dumps(out), flush=True)
@@ -62,6 +67,7 @@ if __name__ == "__main__":
         steps = int(args[i + 1])
         del args[i:i + 2]
     user_order = "--user-order" in args
-    args = [a for a in args if a != "--user-order"]
+    graphs = "--graphs" in args
+    args = [a for a in args if a not in ("--user-order", "--graphs")]
     for c in (args or ["stmv", "water12m"]):
-        run(c, steps, grid_order=not user_order)
+        run(c, steps, grid_order=not user_order, graphs=graphs)
