@@ -207,6 +207,7 @@ NBX_API int nbx_create(int device, const nbx_params* p, nbx_ctx** out)
     // Row f2 (list sorting by length) is available but off by default: on the
     // 12M box the longest-first order costs L2 locality (force kernel +6%), and the tail it
     // removes is ~3% (ncu sm__cycles_active min/max) -- see DESIGN.md section 5
+    if (const char* pk = std::getenv("NBX_PRUNE_KERNEL")) ctx->prune_kernel = std::atoi(pk);
     if (const char* eo = std::getenv("NBX_ENTRY_ORDER")) ctx->entry_order = std::atoi(eo);
     if (const char* fs = std::getenv("NBX_FORCE_SPLIT")) ctx->force_split = std::atoi(fs);
     *out = ctx;

@@ -462,6 +462,86 @@ __global__ void __launch_bounds__(PRUNE_THREADS) k_prune(PruneArgs A)
     }
 }
 
+// Warp-uniform prune: one sci entry per warp, lane = i atom (i-cluster lane/4, row lane%4).
+// The 32 cj entries of a chunk are staged in shared memory (8 coalesced 128-B loads), then
+// every entry is tested by the whole warp at once: 8 r^2 tests per lane, two ballots give the
+// entry's surviving i-cluster bits.  No lane diverges (k_prune's lane-per-entry loop runs
+// the worst lane's early exit for all 32), so the warp issues ~8 instructions per lane per
+// tested atom pair.  Same r^2 rounding and the same keep rule as k_prune: bit-identical lists.
+__global__ void __launch_bounds__(PRUNE_THREADS) k_prune_lanes(PruneArgs A)
+{
+    __shared__ float4 s_xj[PRUNE_THREADS / 32][32][8];
+    const int lane = threadIdx.x & 31;
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int e = A.part + A.nparts * w;
+    if (e >= A.n_sci) return;
+    const unsigned full = 0xffffffffu, lt = (1u << lane) - 1u;
+    const nbx_sci_entry se = A.sci[e];
+    const float3 v = shift_vec(se.shift, A.box);
+    const float4 t0 = A.xq_i[32 * se.sci + lane];
+    const float ax = __fadd_rn(t0.x, v.x), ay = __fadd_rn(t0.y, v.y), az = __fadd_rn(t0.z, v.z);
+    const int kk = lane >> 2, ii = lane & 3;
+    float4(*xs)[8] = s_xj[threadIdx.x >> 5];
+    int kept = 0;
+    for (int c0 = se.cj_start; c0 < se.cj_end; c0 += 32) {
+        const int cnt = min(32, se.cj_end - c0);
+        nbx_cj_entry my;
+        my.cj = 0;
+        my.meta = 0u;
+        if (lane < cnt) my = A.cj[c0 + lane];
+        __syncwarp();
+        for (int r = 0; r < 8 && 4 * r < cnt; r++) {
+            const int t = 4 * r + (lane >> 3);
+            const int cjt = __shfl_sync(full, my.cj, t);
+            if (t < cnt) xs[t][lane & 7] = A.xq_j[8 * cjt + (lane & 7)];
+        }
+        __syncwarp();
+        unsigned my_nm = 0u;
+        for (int t = 0; t < cnt; t++) {
+            const unsigned meta = __shfl_sync(full, my.meta, t);
+            const unsigned pidx = meta >> 8;
+            bool hit = false;
+            if (pidx == 0u) {
+#pragma unroll
+                for (int j = 0; j < 8; j++) {
+                    const float4 b = xs[t][j];
+                    const float dx = __fsub_rn(ax, b.x);
+                    const float dy = __fsub_rn(ay, b.y);
+                    const float dz = __fsub_rn(az, b.z);
+                    hit |= __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx))) < A.rli2;
+                }
+            } else {
+                const unsigned row = ((A.pool[pidx].m[kk][0] | A.pool[pidx].m[kk][1]) >> (8 * ii)) & 0xffu;
+#pragma unroll
+                for (int j = 0; j < 8; j++) {
+                    const float4 b = xs[t][j];
+                    const float dx = __fsub_rn(ax, b.x);
+                    const float dy = __fsub_rn(ay, b.y);
+                    const float dz = __fsub_rn(az, b.z);
+                    const float r2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
+                    hit |= ((row >> j) & 1u) && (r2 < A.rli2);
+                }
+            }
+            const unsigned bits = __ballot_sync(full, hit);
+            const unsigned nm = __ballot_sync(full, lane < 8 && ((bits >> (4 * (lane & 7))) & 0xfu)) & meta & 0xffu;
+            if (lane == t) my_nm = nm;
+        }
+        const unsigned keep = __ballot_sync(full, my_nm != 0u);
+        if (my_nm) {
+            nbx_cj_entry o;
+            o.cj = my.cj;
+            o.meta = my_nm | (my.meta & ~0xffu);
+            A.cj_in[se.cj_start + kept + __popc(keep & lt)] = o;
+        }
+        kept += __popc(keep);
+    }
+    if (lane == 0) {
+        nbx_sci_entry o = se;
+        o.cj_end = se.cj_start + kept;
+        A.sci_in[e] = o;
+    }
+}
+
 // count interacting in-cut-off pairs and pair slots of the inner list (bench denominator)
 __global__ void __launch_bounds__(256) k_count_pairs(PruneArgs A, float rc2, unsigned long long* out)
 {
@@ -575,7 +655,9 @@ void prune(nbx_ctx* ctx, int l, int part, int nparts, cudaStream_t st)
     A.nparts = nparts;
     const int nw = (int)((L.n_sci - part + nparts - 1) / nparts);
     if (nw <= 0) return;
-    k_prune<<<(nw * 32 + PRUNE_THREADS - 1) / PRUNE_THREADS, PRUNE_THREADS, 0, st>>>(A);
+    const int blocks = (nw * 32 + PRUNE_THREADS - 1) / PRUNE_THREADS;
+    if (ctx->prune_kernel == 0) k_prune<<<blocks, PRUNE_THREADS, 0, st>>>(A);
+    else k_prune_lanes<<<blocks, PRUNE_THREADS, 0, st>>>(A);
     ctx->launches++;
     NBX_CUDA(cudaGetLastError());
     if (ctx->entry_order) sort_entries(ctx, L, st);
