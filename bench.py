@@ -358,8 +358,22 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def _json_only_stdout():
+    """Keep stdout for the JSON line alone: native libraries that write to fd 1 (NCCL's
+    version banner under NCCL_DEBUG, cuFFT/driver notices) are sent to stderr, Python's
+    sys.stdout keeps the original descriptor."""
+    try:
+        sys.stdout.flush()
+        keep = os.dup(1)
+        os.dup2(2, 1)
+        sys.stdout = os.fdopen(keep, "w", buffering=1)
+    except OSError:
+        pass
+
+
 def main():
     args = parse()
+    _json_only_stdout()
     # no cyclic-GC pauses inside timed regions (a gen-2 pass during a Python-side search /
     # repartition step stalls the GPU that step waits on); reference counting still frees
     gc.collect()
