@@ -422,6 +422,10 @@ NBX_API int nbx_get_f(nbx_ctx* ctx, int grid, float* f, int accumulate, void* st
     NBX_GUARD_END
 }
 
+// cached step graphs per context and kind (a caller that allocates fresh x / f tensors every
+// step would otherwise grow the cache without bound)
+static constexpr size_t kMaxStepGraphs = 16;
+
 // X op (+ prune) + force + F op of a non-search MD step of the LOCAL list as one graph
 // launch.  Captured (relaxed mode, on a private stream: nothing executes during capture)
 // on first use for (x, f, what) and refreshed in place after anything bumped ctx->epoch.
@@ -465,6 +469,10 @@ NBX_API int nbx_step_graph(nbx_ctx* ctx, const float* x, float* f, uint32_t what
                 cudaGraphExecDestroy(g->exec);
             }
         } else {
+            if (ctx->graphs.size() >= kMaxStepGraphs) { // callers cycling buffers: drop the oldest
+                cudaGraphExecDestroy(ctx->graphs.front().exec);
+                ctx->graphs.erase(ctx->graphs.begin());
+            }
             ctx->graphs.push_back(nbx_ctx::StepGraph{x, f, what, 0, 0, nullptr});
             g = &ctx->graphs.back();
         }
@@ -540,6 +548,10 @@ NBX_API int nbx_step_graph_pme(nbx_ctx* ctx, nbx_pme* pme, float* x, float* f, f
                 cudaGraphExecDestroy(g->exec);
             }
         } else {
+            if (ctx->full_graphs.size() >= kMaxStepGraphs) {
+                cudaGraphExecDestroy(ctx->full_graphs.front().exec);
+                ctx->full_graphs.erase(ctx->full_graphs.begin());
+            }
             ctx->full_graphs.push_back(nbx_ctx::FullGraph{pme, 0, x, f, v, inv_mass, dt, what, 0, 0, nullptr});
             g = &ctx->full_graphs.back();
         }

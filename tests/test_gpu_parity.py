@@ -356,6 +356,24 @@ def test_graph_steps_match_eager(gpu):
     assert nb_g.launch_count() - l0 >= 67 * 3  # graph replays count their kernel nodes
 
 
+def test_graph_cache_bounded(gpu):
+    """A caller passing a fresh force tensor every step: the per-context graph cache evicts
+    its oldest graph (16 kept) and every replay still gives the eager forces."""
+    import torch
+    s = get_system("water3k")
+    nb = gpu_nb(s)
+    x = to_dev(s.x)
+    fe = torch.empty_like(x)
+    nb.step(x, fe, 0)
+    fe2 = torch.empty_like(x)
+    nb.step(x, fe2, 1)
+    for step in range(1, 40):
+        fg = torch.empty_like(x)
+        nb.step(x, fg, step if step % 10 else step + 1, graphs=True)
+        torch.cuda.synchronize()
+        assert float((fg - fe2).abs().max()) < 1e-3 * float(fe2.abs().max()), step
+
+
 @pytest.mark.parametrize("natoms", [60000, None])
 @pytest.mark.parametrize("config", ["stmv_fsw", "stmv_tab"])
 def test_force_switch_flavour(gpu, natoms, config):
