@@ -127,7 +127,7 @@ struct nbx_ctx {
     nbx::DBuf<int> counter;   // work counters [8]
     int64_t launches = 0;
     int force_split = 0; // > 0: fixed work items per sci entry (env NBX_FORCE_SPLIT), 0: auto
-    int prune_kernel = 0; // 0: k_prune (lane per cj entry), 1: k_prune_lanes (lane per i atom, slower on large boxes); env NBX_PRUNE_KERNEL
+    int prune_kernel = 2; // 0: k_prune (lane per cj entry), 1: k_prune_lanes (lane per i atom), 2: k_prune_packed (compacted tiles, FP32x2); env NBX_PRUNE_KERNEL
     int entry_order = 0; // 0: list order (spatially coherent), 1: longest first (env NBX_ENTRY_ORDER)
     // nbx_step_graph: natively captured X op (+ prune) + force + F op, one per (x, f, what);
     // `epoch` is bumped by every call that can move list/grid buffers or change constants,

@@ -21,6 +21,7 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include "f32x2.cuh"
 #include "nbx_internal.cuh"
 
 namespace nbx {
@@ -542,6 +543,146 @@ __global__ void __launch_bounds__(PRUNE_THREADS) k_prune_lanes(PruneArgs A)
     }
 }
 
+// Packed prune: the active (cj entry, i-cluster) tiles of a 32-entry chunk -- the outer
+// list's imask bits, ~5 of 8 per entry -- are compacted into an item table in shared memory
+// and tested 8 tiles per warp pass (4 lanes = the tile's 4 i atoms, 8 j atoms each).  Unlike
+// k_prune_lanes it never tests a tile the outer list excluded, and unlike k_prune no lane
+// waits on another lane's entry.  The j atoms are staged structure-of-arrays so an unmasked
+// pass runs two j atoms per FADD2 / FMUL2 / FFMA2 (the kernel is issue-bound with the FP32
+// pipe half idle).  dx = xj - xi is the exact negation of xi - xj, so every r^2 has the
+// scalar kernels' rounding and the keep rule is unchanged: bit-identical lists.
+constexpr int PRUNE_JS = 28; // per-entry stride (floats): x[8] y[8] z[8] + pad (bank groups)
+
+__global__ void __launch_bounds__(PRUNE_THREADS) k_prune_packed(PruneArgs A)
+{
+    constexpr int W = PRUNE_THREADS / 32;
+    __shared__ __align__(16) float s_xj[W][32][PRUNE_JS];
+    __shared__ float4 s_xi[W][32];
+    __shared__ unsigned s_nm[W][32];
+    __shared__ unsigned s_pidx[W][32];
+    __shared__ unsigned char s_item[W][256]; // entry << 3 | i-cluster
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int e = A.part + A.nparts * w;
+    if (e >= A.n_sci) return;
+    const unsigned full = 0xffffffffu, lt = (1u << lane) - 1u;
+    const nbx_sci_entry se = A.sci[e];
+    {
+        const float3 v = shift_vec(se.shift, A.box);
+        const float4 t0 = A.xq_i[32 * se.sci + lane];
+        s_xi[wib][lane] = make_float4(__fadd_rn(t0.x, v.x), __fadd_rn(t0.y, v.y), __fadd_rn(t0.z, v.z), 0.f);
+    }
+    const int g = lane >> 2, ii = lane & 3;
+    int kept = 0;
+    for (int c0 = se.cj_start; c0 < se.cj_end; c0 += 32) {
+        const int cnt = min(32, se.cj_end - c0);
+        nbx_cj_entry my;
+        my.cj = 0;
+        my.meta = 0u;
+        if (lane < cnt) my = A.cj[c0 + lane];
+        __syncwarp();
+        for (int r = 0; r < 8 && 4 * r < cnt; r++) {
+            const int t = 4 * r + (lane >> 3);
+            const int cjt = __shfl_sync(full, my.cj, t);
+            if (t < cnt) {
+                const int j = lane & 7;
+                const float4 b = A.xq_j[8 * cjt + j];
+                s_xj[wib][t][j] = b.x;
+                s_xj[wib][t][8 + j] = b.y;
+                s_xj[wib][t][16 + j] = b.z;
+            }
+        }
+        // item table: exclusive scan of the entries' active-tile counts
+        const unsigned imask = my.meta & 0xffu;
+        const int pc = __popc(imask);
+        int incl = pc;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int y = __shfl_up_sync(full, incl, d);
+            if (lane >= d) incl += y;
+        }
+        const int total = __shfl_sync(full, incl, 31);
+        {
+            unsigned mm = imask;
+            int o = incl - pc;
+            while (mm) {
+                s_item[wib][o++] = (unsigned char)((lane << 3) | (__ffs(mm) - 1));
+                mm &= mm - 1u;
+            }
+        }
+        s_nm[wib][lane] = 0u;
+        s_pidx[wib][lane] = my.meta >> 8;
+        __syncwarp();
+        for (int base = 0; base < total; base += 8) {
+            const int m = base + g;
+            const unsigned it = m < total ? s_item[wib][m] : 0u;
+            const int t = it >> 3, kk = it & 7;
+            const float4 a = s_xi[wib][4 * kk + ii];
+            const unsigned pidx = s_pidx[wib][t];
+            const float* xs = s_xj[wib][t];
+            bool hit = false;
+            if (!__any_sync(full, pidx != 0u)) {
+                const f2x AX = bc(a.x), AY = bc(a.y), AZ = bc(a.z);
+                float r2min = 0.f;
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+                    const ulonglong2 X = *reinterpret_cast<const ulonglong2*>(xs + 4 * h);
+                    const ulonglong2 Y = *reinterpret_cast<const ulonglong2*>(xs + 8 + 4 * h);
+                    const ulonglong2 Z = *reinterpret_cast<const ulonglong2*>(xs + 16 + 4 * h);
+                    const f2x DX0 = sub2(X.x, AX), DY0 = sub2(Y.x, AY), DZ0 = sub2(Z.x, AZ);
+                    const f2x DX1 = sub2(X.y, AX), DY1 = sub2(Y.y, AY), DZ1 = sub2(Z.y, AZ);
+                    const float2 R0 = upk(fma2(DZ0, DZ0, fma2(DY0, DY0, mul2(DX0, DX0))));
+                    const float2 R1 = upk(fma2(DZ1, DZ1, fma2(DY1, DY1, mul2(DX1, DX1))));
+                    const float m4 = fminf(fminf(R0.x, R0.y), fminf(R1.x, R1.y));
+                    r2min = h ? fminf(r2min, m4) : m4;
+                }
+                hit = r2min < A.rli2;
+            } else {
+                // a pass holding an excluded (pool) tile: the same packed r^2, with masked
+                // pairs' r^2 replaced by +inf before the minimum
+                unsigned row = 0xffu;
+                if (pidx) row = ((A.pool[pidx].m[kk][0] | A.pool[pidx].m[kk][1]) >> (8 * ii)) & 0xffu;
+                const f2x AX = bc(a.x), AY = bc(a.y), AZ = bc(a.z);
+                float r2min = 0.f;
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+                    const ulonglong2 X = *reinterpret_cast<const ulonglong2*>(xs + 4 * h);
+                    const ulonglong2 Y = *reinterpret_cast<const ulonglong2*>(xs + 8 + 4 * h);
+                    const ulonglong2 Z = *reinterpret_cast<const ulonglong2*>(xs + 16 + 4 * h);
+                    const f2x DX0 = sub2(X.x, AX), DY0 = sub2(Y.x, AY), DZ0 = sub2(Z.x, AZ);
+                    const f2x DX1 = sub2(X.y, AX), DY1 = sub2(Y.y, AY), DZ1 = sub2(Z.y, AZ);
+                    const float2 R0 = upk(fma2(DZ0, DZ0, fma2(DY0, DY0, mul2(DX0, DX0))));
+                    const float2 R1 = upk(fma2(DZ1, DZ1, fma2(DY1, DY1, mul2(DX1, DX1))));
+                    const unsigned rb = row >> (4 * h);
+                    const float inf = __int_as_float(0x7f800000);
+                    const float m4 = fminf(fminf((rb & 1u) ? R0.x : inf, (rb & 2u) ? R0.y : inf),
+                                           fminf((rb & 4u) ? R1.x : inf, (rb & 8u) ? R1.y : inf));
+                    r2min = h ? fminf(r2min, m4) : m4;
+                }
+                hit = r2min < A.rli2;
+            }
+            const unsigned bits = __ballot_sync(full, hit && m < total);
+            if (ii == 0 && ((bits >> (4 * g)) & 0xfu)) atomicOr(&s_nm[wib][t], 1u << kk);
+        }
+        __syncwarp();
+        const unsigned my_nm = lane < cnt ? s_nm[wib][lane] : 0u;
+        const unsigned keep = __ballot_sync(full, my_nm != 0u);
+        if (my_nm) {
+            nbx_cj_entry o;
+            o.cj = my.cj;
+            o.meta = my_nm | (my.meta & ~0xffu);
+            A.cj_in[se.cj_start + kept + __popc(keep & lt)] = o;
+        }
+        kept += __popc(keep);
+        __syncwarp();
+    }
+    if (lane == 0) {
+        nbx_sci_entry o = se;
+        o.cj_end = se.cj_start + kept;
+        A.sci_in[e] = o;
+    }
+}
+
 // count interacting in-cut-off pairs and pair slots of the inner list (bench denominator)
 __global__ void __launch_bounds__(256) k_count_pairs(PruneArgs A, float rc2, unsigned long long* out)
 {
@@ -657,7 +798,8 @@ void prune(nbx_ctx* ctx, int l, int part, int nparts, cudaStream_t st)
     if (nw <= 0) return;
     const int blocks = (nw * 32 + PRUNE_THREADS - 1) / PRUNE_THREADS;
     if (ctx->prune_kernel == 0) k_prune<<<blocks, PRUNE_THREADS, 0, st>>>(A);
-    else k_prune_lanes<<<blocks, PRUNE_THREADS, 0, st>>>(A);
+    else if (ctx->prune_kernel == 1) k_prune_lanes<<<blocks, PRUNE_THREADS, 0, st>>>(A);
+    else k_prune_packed<<<blocks, PRUNE_THREADS, 0, st>>>(A); // default
     ctx->launches++;
     NBX_CUDA(cudaGetLastError());
     if (ctx->entry_order) sort_entries(ctx, L, st);

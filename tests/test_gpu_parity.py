@@ -109,13 +109,13 @@ def test_prune_after_motion(gpu, name):
 
 @pytest.mark.parametrize("name", ["rnase24k", "water3k"])
 def test_prune_kernels_identical(gpu, name, monkeypatch):
-    """Both prune kernels (NBX_PRUNE_KERNEL=0: lane per cj entry, 1: lane per i atom,
-    opt-in) give the oracle's inner list bit-exactly after motion, whole and rolling."""
+    """All prune kernels (NBX_PRUNE_KERNEL=0: lane per cj entry, 1: lane per i atom, 2: packed
+    active tiles) give the oracle's inner list bit-exactly after motion, whole and rolling."""
     s = get_system(name)
     rng = np.random.default_rng(11)
     x1 = (s.x + rng.uniform(-0.04, 0.04, size=s.x.shape)).astype(np.float32)
     lists = []
-    for kern in ("0", "1"):
+    for kern in ("0", "1", "2"):
         monkeypatch.setenv("NBX_PRUNE_KERNEL", kern)
         nb, on, xd = run_pair(s)
         nb.put_x(to_dev(x1))
@@ -124,7 +124,7 @@ def test_prune_kernels_identical(gpu, name, monkeypatch):
         lists.append(nb.pairlist(1))
     on.put_x(x1)
     on.prune()
-    for kern, lg in zip("01", lists):
+    for kern, lg in zip("012", lists):
         assert_lists_equal(lg, on.list.export(1), f"{name} prune kernel {kern}")
 
 
