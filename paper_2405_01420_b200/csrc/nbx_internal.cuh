@@ -101,6 +101,7 @@ struct ForceConsts {
     float rc2_big;   // rc2 * 2^64: cut-off step as one FFMA.SAT (force-only kernels)
     unsigned one;    // 1, opaque to the compiler: integer adds issued as IMAD (FMA pipe)
     float ewn[6], ewd[5]; // F-only Ewald: -beta^3 G as N(r2) / D(r2), D monic (pairmath.cuh)
+    alignas(8) float ewnd[10]; // (ewn[k], ewd[k]) interleaved: one 64-bit constant per FFMA2
 };
 
 } // namespace nbx
