@@ -16,7 +16,7 @@ LIB = os.path.join(HERE, "libnbx.so")
 ROOT = os.path.dirname(HERE)
 
 SOURCES = ["capi.cu", "grid.cu", "search.cu", "force.cu", "bufops.cu", "peer.cu", "pme.cu"]
-HEADERS = ["nbx_internal.cuh", "pairmath.cuh"]
+HEADERS = ["nbx_internal.cuh", "pairmath.cuh", "f32x2.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
               "--expt-relaxed-constexpr", f"-I{os.path.join(ROOT, 'include')}"]
