@@ -139,7 +139,7 @@ def pme(x, q, box, beta, epsfac, nk=None, order=4):
     for a in range(3):
         for b in range(3):
             vir[a, b] = -0.5 * float((Em * ((1.0 if a == b else 0.0) - fac * comps[a] * comps[b])).sum())
-    phi = np.fft.irfftn(G * S, s=nk) * (Kx * Ky * Kz)
+    phi = np.fft.irfftn(G * S, s=nk, axes=(0, 1, 2)) * (Kx * Ky * Kz)
     # gather (pme_gather)
     P = phi[ix[:, :, None, None], iy[:, None, :, None], iz[:, None, None, :]]  # [N, o, o, o]
     tx, ty, tz = theta[:, 0], theta[:, 1], theta[:, 2]
