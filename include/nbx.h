@@ -214,8 +214,13 @@ NBX_API int nbx_step_graph(nbx_ctx* ctx, const float* x_dev, float* f_dev, uint3
  *   nbx_peer_halo_x (wait + gather halo x over NVLink into grid 1) -> nonlocal prune ->
  *   nbx_peer_force_nonlocal (j forces red.add'ed into the owners' inboxes + signal) ->
  *   nbx_peer_get_f (wait + grid-0 F op + inbox)
- * with one monotonically increasing `seq` per step, identical on all ranks.  Waits are
- * bounded (env NBX_PEER_TIMEOUT_S, default 30): nbx_peer_status reports a timeout.        */
+ * with one monotonically increasing `seq` per step, identical on all ranks.  `flags`
+ * (NBX_FORCE_ENERGY | NBX_FORCE_VIRIAL, after nbx_clear_energies) make it an energy /
+ * virial step: the nonlocal kernel accumulates energies and the halo atoms' x (x) f is
+ * summed before the push, the home atoms' before the inbox is added, so nbx_energies
+ * (after nbx_peer_get_f here) returns this rank's share and an all-reduce gives the total.
+ * Waits are bounded (env NBX_PEER_TIMEOUT_S, default 30): on a timeout the wait kernel
+ * records it (nbx_peer_status) and traps -- the context is lost, the step fails loudly.   */
 #define NBX_PEER_HANDLE_BYTES 64
 NBX_API int nbx_peer_init(nbx_ctx* ctx, int32_t rank, int32_t world, int32_t capacity, void* handle_out);
 NBX_API int nbx_peer_open(nbx_ctx* ctx, const void* handles /* world * NBX_PEER_HANDLE_BYTES */);
@@ -223,8 +228,8 @@ NBX_API int nbx_peer_set_halo(nbx_ctx* ctx, int32_t n_halo, const int32_t* owner
                               const float* shift_dev /* [n_halo][3] */, void* stream);
 NBX_API int nbx_peer_put_x(nbx_ctx* ctx, const float* x_home_dev, uint32_t seq, void* stream);
 NBX_API int nbx_peer_halo_x(nbx_ctx* ctx, uint32_t seq, void* stream);
-NBX_API int nbx_peer_force_nonlocal(nbx_ctx* ctx, uint32_t seq, void* stream);
-NBX_API int nbx_peer_get_f(nbx_ctx* ctx, float* f_home_dev, uint32_t seq, void* stream);
+NBX_API int nbx_peer_force_nonlocal(nbx_ctx* ctx, uint32_t seq, uint32_t flags, void* stream);
+NBX_API int nbx_peer_get_f(nbx_ctx* ctx, float* f_home_dev, uint32_t seq, uint32_t flags, void* stream);
 NBX_API int nbx_peer_status(nbx_ctx* ctx, int32_t* timed_out);
 
 /* Energies and virial accumulated since the last clear.  Reads grid buffers, so call it

@@ -258,11 +258,31 @@ NBX_API int nbx_set_topology(nbx_ctx* ctx, int32_t n, const float* q, const int3
         return fail(NBX_EINVAL, "too many LJ types for the shared-memory table (max 78)");
     for (int a = 0; a < n; a++)
         if (type[a] < 0 || type[a] >= ntypes) return fail(NBX_EINVAL, "atom type out of range");
+    {
+        // force kernel shared memory: the LJ table (+ the EWALD_TAB force and potential tables)
+        const bool comb = ctx->p.lj_modifier == NBX_LJ_COMB_GEOM || ctx->p.lj_modifier == NBX_LJ_COMB_LB;
+        const size_t tab = ctx->p.coulomb_type == NBX_COULOMB_EWALD_TAB ? 2 * (size_t)ctx->c.tab_n : 0;
+        if (((comb ? (size_t)ntypes : (size_t)ntypes * ntypes) + tab) * sizeof(float2) > FORCE_SMEM_MAX)
+            return fail(NBX_EINVAL, "LJ + Ewald tables exceed the force kernel's shared-memory opt-in");
+    }
     const int nexcl = excl_offsets[n];
     if (excl_offsets[0] != 0 || nexcl < 0 || (nexcl > 0 && !excl_gids))
         return fail(NBX_EINVAL, "bad exclusion CSR");
+    // offsets monotone and inside [0, nexcl] (the search's mask builder walks them unchecked)
+    for (int a = 0; a < n; a++)
+        if (excl_offsets[a] > excl_offsets[a + 1] || excl_offsets[a + 1] > nexcl)
+            return fail(NBX_EINVAL, "exclusion CSR offsets are not monotone / exceed the id count");
     for (int e = 0; e < nexcl; e++)
         if (excl_gids[e] < 0 || excl_gids[e] >= n) return fail(NBX_EINVAL, "exclusion id out of range");
+    // symmetry: b in excl(a) <=> a in excl(b); otherwise a tile's masks would depend on which
+    // atom of the pair lands in the i-cluster
+    for (int a = 0; a < n; a++)
+        for (int e = excl_offsets[a]; e < excl_offsets[a + 1]; e++) {
+            const int b = excl_gids[e];
+            bool found = false;
+            for (int k = excl_offsets[b]; k < excl_offsets[b + 1] && !found; k++) found = excl_gids[k] == a;
+            if (!found) return fail(NBX_EINVAL, "exclusion CSR is not symmetric");
+        }
     ctx->natoms_global = n;
     ctx->ntypes = ntypes;
     const int nn = n > 0 ? n : 1;
@@ -627,21 +647,23 @@ NBX_API int nbx_peer_halo_x(nbx_ctx* ctx, uint32_t seq, void* stream)
     NBX_GUARD_END
 }
 
-NBX_API int nbx_peer_force_nonlocal(nbx_ctx* ctx, uint32_t seq, void* stream)
+NBX_API int nbx_peer_force_nonlocal(nbx_ctx* ctx, uint32_t seq, uint32_t flags, void* stream)
 {
     NBX_GUARD_BEGIN
     NBX_CHECK_CTX(ctx);
-    peer_force_nonlocal(ctx, seq, (cudaStream_t)stream);
+    if (flags & ~(uint32_t)(NBX_FORCE_ENERGY | NBX_FORCE_VIRIAL)) return fail(NBX_EINVAL, "bad force flags");
+    peer_force_nonlocal(ctx, seq, flags, (cudaStream_t)stream);
     return NBX_OK;
     NBX_GUARD_END
 }
 
-NBX_API int nbx_peer_get_f(nbx_ctx* ctx, float* f_home, uint32_t seq, void* stream)
+NBX_API int nbx_peer_get_f(nbx_ctx* ctx, float* f_home, uint32_t seq, uint32_t flags, void* stream)
 {
     NBX_GUARD_BEGIN
     NBX_CHECK_CTX(ctx);
     if (!f_home && ctx->grid[0].n > 0) return fail(NBX_EINVAL, "null force buffer");
-    peer_get_f(ctx, f_home, seq, (cudaStream_t)stream);
+    if (flags & ~(uint32_t)(NBX_FORCE_ENERGY | NBX_FORCE_VIRIAL)) return fail(NBX_EINVAL, "bad force flags");
+    peer_get_f(ctx, f_home, seq, flags, (cudaStream_t)stream);
     return NBX_OK;
     NBX_GUARD_END
 }
@@ -661,6 +683,7 @@ NBX_API int nbx_clear_energies(nbx_ctx* ctx, void* stream)
     NBX_GUARD_BEGIN
     NBX_CHECK_CTX(ctx);
     NBX_CUDA(cudaMemsetAsync(ctx->acc.p, 0, sizeof(double) * (2 + 3 * NBX_NSHIFT + 9), (cudaStream_t)stream));
+    ctx->xf_done = 0;
     return NBX_OK;
     NBX_GUARD_END
 }
@@ -671,9 +694,15 @@ NBX_API int nbx_energies(nbx_ctx* ctx, double* e, double* vir, void* stream)
     NBX_CHECK_CTX(ctx);
     cudaStream_t st = (cudaStream_t)stream;
     const int NA = 2 + 3 * NBX_NSHIFT + 9;
-    NBX_CUDA(cudaMemsetAsync(ctx->acc.p + 2 + 3 * NBX_NSHIFT, 0, sizeof(double) * 9, st));
-    virial_sum(ctx, 0, st);
-    if (ctx->list[1].built) virial_sum(ctx, 1, st);
+    if (ctx->xf_done) {
+        // peer-halo energy step: both grids' x (x) f were summed before their forces moved
+        if (ctx->xf_done != 3u) return fail(NBX_EINVAL, "peer energy step incomplete (virial of one grid missing)");
+    } else {
+        NBX_CUDA(cudaMemsetAsync(ctx->acc.p + 2 + 3 * NBX_NSHIFT, 0, sizeof(double) * 9, st));
+        virial_sum(ctx, 0, st);
+        if (ctx->list[1].built) virial_sum(ctx, 1, st);
+    }
+    ctx->xf_done = 0;
     double h[2 + 3 * NBX_NSHIFT + 9];
     double q2 = 0.0;
     NBX_CUDA(cudaMemcpyAsync(h, ctx->acc.p, sizeof(double) * NA, cudaMemcpyDeviceToHost, st));

@@ -13,6 +13,9 @@
 #define NBX_FILLER_COORD (-1.0e5f)
 #define NBX_BB_EMPTY 1.0e30f
 #define NBX_R2MIN 1.0e-6f
+// dynamic shared memory opted into by the force kernels (LJ table + EWALD_TAB tables);
+// nbx_set_topology rejects tables that would not fit
+#define FORCE_SMEM_MAX (96 * 1024)
 
 namespace nbx {
 
@@ -142,6 +145,9 @@ struct nbx_ctx {
         cudaGraphExec_t exec;
     };
     nbx::Peer* peer = nullptr;
+    // peer-halo energy steps: x (x) f already summed per grid (bit 0: grid 0, bit 1: grid 1)
+    // by nbx_peer_get_f / nbx_peer_force_nonlocal, so nbx_energies must not re-sum it
+    unsigned xf_done = 0;
     uint64_t epoch = 1;
     std::vector<StepGraph> graphs;
     // nbx_step_graph_pme: the same plus PME on grid 0 and the leap-frog update, keyed by all
@@ -231,8 +237,8 @@ void peer_open(nbx_ctx* ctx, const void* handles);
 void peer_set_halo(nbx_ctx* ctx, int n, const int* owner, const int* home, const float* shift, cudaStream_t st);
 void peer_put_x(nbx_ctx* ctx, const float* x, unsigned seq, cudaStream_t st);
 void peer_halo_x(nbx_ctx* ctx, unsigned seq, cudaStream_t st);
-void peer_force_nonlocal(nbx_ctx* ctx, unsigned seq, cudaStream_t st);
-void peer_get_f(nbx_ctx* ctx, float* f, unsigned seq, cudaStream_t st);
+void peer_force_nonlocal(nbx_ctx* ctx, unsigned seq, unsigned flags, cudaStream_t st);
+void peer_get_f(nbx_ctx* ctx, float* f, unsigned seq, unsigned flags, cudaStream_t st);
 int peer_status(nbx_ctx* ctx);
 ForceConsts make_force_consts(const nbx_consts& c);
 void pme_setup(nbx_pme* pme);

@@ -20,7 +20,14 @@
 // Flags are per-rank uint32 sequence numbers: rank r's region holds flags[2][world], written
 // by rank w with st.release.sys at [kind][w] and spun on with ld.acquire.sys by r.  The spin
 // is bounded (NBX_PEER_TIMEOUT_S, default 30 s): a missing peer sets an error word that
-// nbx_peer_status reports instead of hanging the GPU.
+// nbx_peer_status reports and then traps, so a timed-out step can never go on to read stale
+// or half-written peer memory (the CUDA context is lost and every later call fails loudly).
+//
+// Energy / virial steps run through the same halo (flags NBX_FORCE_ENERGY / VIRIAL): the
+// virial sum x (x) f of the halo atoms is taken on the importing rank from grid 1's cluster
+// forces (halo coordinates in this rank's frame) BEFORE they are pushed to the owners, and the
+// home atoms' sum from grid 0 BEFORE the inbox is added, so each cross-domain pair enters
+// exactly one rank's virial -- the single-sum form of -1/2 sum_pairs r_ij (x) f_ij.
 #include <cstdlib>
 #include <cstring>
 
@@ -78,7 +85,8 @@ __global__ void k_peer_wait(const unsigned* flags, int world, int kind, unsigned
         if ((int)(v - seq) >= 0) break;
         if (gtimer() - t0 > timeout_ns) {
             atomicExch(err, 1);
-            break;
+            __threadfence_system();
+            __trap(); // fatal: the step must not consume stale peer memory
         }
         __nanosleep(128);
     }
@@ -243,6 +251,7 @@ void peer_set_halo(nbx_ctx* ctx, int n, const int* owner, const int* home, const
     if (G1.n != n) throw CudaError{cudaErrorInvalidValue, "n_halo differs from the grid-1 atom count"};
     if (G0.n > P.cap) throw CudaError{cudaErrorInvalidValue, "home atoms exceed the peer capacity"};
     P.n_halo = n;
+    NBX_CUDA(cudaMemsetAsync(P.err.p, 0, sizeof(int), st));
     P.src.ensure(n > 0 ? n : 1);
     P.dst.ensure(n > 0 ? n : 1);
     P.hshift.ensure(n > 0 ? n : 1);
@@ -304,14 +313,19 @@ void peer_halo_x(nbx_ctx* ctx, unsigned seq, cudaStream_t st)
     }
 }
 
-void peer_force_nonlocal(nbx_ctx* ctx, unsigned seq, cudaStream_t st)
+void peer_force_nonlocal(nbx_ctx* ctx, unsigned seq, unsigned flags, cudaStream_t st)
 {
     Peer& P = need(ctx, true, true);
     Grid& G = ctx->grid[1];
-    if (P.fused) {
+    if (P.fused && !flags) {
         if (ctx->list[1].built && ctx->list[1].n_sci > 0) force(ctx, 1, 0, st, P.fj_dst.p);
     } else {
-        if (ctx->list[1].built && ctx->list[1].n_sci > 0) force(ctx, 1, 0, st);
+        if (ctx->list[1].built && ctx->list[1].n_sci > 0) force(ctx, 1, flags, st);
+        if (flags & NBX_FORCE_VIRIAL) {
+            // halo atoms' x (x) f while their forces are still here (section header)
+            virial_sum(ctx, 1, st);
+            ctx->xf_done |= 2;
+        }
         if (G.n > 0) {
             k_peer_push<<<(G.n + 255) / 256, 256, 0, st>>>(G.n, G.islot.p, G.f.p, P.dst.p);
             ctx->launches++;
@@ -322,9 +336,15 @@ void peer_force_nonlocal(nbx_ctx* ctx, unsigned seq, cudaStream_t st)
     signal(ctx, P, 1, seq, st);
 }
 
-void peer_get_f(nbx_ctx* ctx, float* f, unsigned seq, cudaStream_t st)
+void peer_get_f(nbx_ctx* ctx, float* f, unsigned seq, unsigned flags, cudaStream_t st)
 {
     Peer& P = need(ctx, true, true);
+    if (flags & NBX_FORCE_VIRIAL) {
+        // home atoms' x (x) f from the forces computed on this rank (local + nonlocal lists),
+        // before the inbox (pairs other ranks computed and count) is added
+        virial_sum(ctx, 0, st);
+        ctx->xf_done |= 1;
+    }
     wait(ctx, P, 1, seq, st);
     Grid& G = ctx->grid[0];
     if (G.n > 0) {

@@ -172,12 +172,12 @@ class NbxEngine:
     def peer_halo_x(self, seq, stream=None):
         self.nbx.check(self.nbx.lib().nbx_peer_halo_x(self.ctx.h, seq, self._st(stream)))
 
-    def peer_force_nonlocal(self, seq, stream=None):
-        self.nbx.check(self.nbx.lib().nbx_peer_force_nonlocal(self.ctx.h, seq, self._st(stream)))
+    def peer_force_nonlocal(self, seq, flags=0, stream=None):
+        self.nbx.check(self.nbx.lib().nbx_peer_force_nonlocal(self.ctx.h, seq, flags, self._st(stream)))
 
-    def peer_get_f(self, f, seq, stream=None):
+    def peer_get_f(self, f, seq, flags=0, stream=None):
         self.nbx.check(self.nbx.lib().nbx_peer_get_f(self.ctx.h, self.nbx._dev_ptr(f) if f.shape[0] else None,
-                                                     seq, self._st(stream)))
+                                                     seq, flags, self._st(stream)))
 
     def peer_status(self):
         import ctypes as C
@@ -238,16 +238,53 @@ class DomainDecomposition:
         # p2p steps: halo gather + nonlocal force on a side stream (NBX_DD_OVERLAP=0 disables)
         self.overlap_nonlocal = os.environ.get("NBX_DD_OVERLAP", "1") != "0"
         self._side = None
+        self._peer_cap = 0
+        # gloo moves host tensors only: with CUDA tensors (e.g. several ranks sharing one GPU,
+        # tests/test_dd_gpu.py's oversubscribed mode) every exchange is staged through host
+        # memory; with NCCL the device tensors go straight onto the wire
+        self._staged = dist.get_backend(group) == "gloo" and self.device.type == "cuda"
 
     # ---------------------------------------------------------------------- partitioning
     def _exchange(self, sends, recvs):
-        """One batched NCCL/gloo point-to-point group: sends/recvs are (tensor, peer) lists."""
+        """One batched NCCL/gloo point-to-point group: sends/recvs are (tensor, peer) lists.
+        Staged (gloo + CUDA tensors): completes before returning, through host copies."""
         dist = self.dist
-        ops = [dist.P2POp(dist.isend, t, p, group=self.group) for t, p in sends if t.numel()]
-        ops += [dist.P2POp(dist.irecv, t, p, group=self.group) for t, p in recvs if t.numel()]
-        if not ops:
+        sends = [(t, p) for t, p in sends if t.numel()]
+        recvs = [(t, p) for t, p in recvs if t.numel()]
+        if not sends and not recvs:
             return []
+        if self._staged:
+            hs = [(t.cpu(), p) for t, p in sends]
+            hr = [(self.torch.empty(t.shape, dtype=t.dtype), p) for t, p in recvs]
+            ops = [dist.P2POp(dist.isend, t, p, group=self.group) for t, p in hs]
+            ops += [dist.P2POp(dist.irecv, t, p, group=self.group) for t, p in hr]
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+            for (t, _), (h, _) in zip(recvs, hr):
+                t.copy_(h)
+            return []
+        ops = [dist.P2POp(dist.isend, t, p, group=self.group) for t, p in sends]
+        ops += [dist.P2POp(dist.irecv, t, p, group=self.group) for t, p in recvs]
         return dist.batch_isend_irecv(ops)
+
+    def _all_reduce(self, t, op=None):
+        """In-place all-reduce (host-staged under gloo with CUDA tensors)."""
+        dist = self.dist
+        op = dist.ReduceOp.SUM if op is None else op
+        if self._staged:
+            h = t.cpu()
+            dist.all_reduce(h, op=op, group=self.group)
+            t.copy_(h)
+        else:
+            dist.all_reduce(t, op=op, group=self.group)
+        return t
+
+    def _all_gather(self, t):
+        dist = self.dist
+        src = t.cpu() if self._staged else t
+        out = [self.torch.empty_like(src) for _ in range(self.world)]
+        dist.all_gather(out, src, group=self.group)
+        return out
 
     def _tick(self, name=None):
         if self.timing is None:
@@ -262,6 +299,7 @@ class DomainDecomposition:
         """Assign home atoms, build the halo plan, grids and lists (a search step)."""
         torch = self.torch
         dev = self.device
+        self.check_peer()
         self._tick()
         box = torch.tensor(self.box, dtype=torch.float32, device=dev)
         xg = x_global.to(dev, torch.float32)
@@ -377,17 +415,27 @@ class DomainDecomposition:
     def _peer_map(self):
         """Peer halo map after a repartition: for every imported atom its owner rank, its index
         in the owner's home order (home atoms are in increasing global id) and its import
-        shift (a multiple of the box edge per dimension)."""
+        shift (a multiple of the box edge per dimension).
+
+        The IPC regions hold `cap` home atoms per rank (the same on all ranks).  Every
+        repartition all-reduces the largest home count; when a rank outgrows `cap` (load
+        imbalance after atoms moved) all ranks re-create and re-exchange their regions at
+        1.25x the new maximum, together, after their outstanding peer traffic has drained."""
         torch, dist = self.torch, self.dist
         dev = self.device
-        if not self._peer_ready:
-            cap = int(math.ceil(1.5 * self.sys.natoms / self.world)) + 4096
+        nmax = torch.tensor([self.n_home], dtype=torch.int64, device=dev)
+        nmax = int(self._all_reduce(nmax, op=dist.ReduceOp.MAX)[0])
+        if not self._peer_ready or nmax > self._peer_cap:
+            cap = max(int(math.ceil(1.5 * self.sys.natoms / self.world)) + 4096, int(math.ceil(1.25 * nmax)))
+            if self._peer_ready:
+                torch.cuda.synchronize(dev)  # nobody still reads / reduces into the old regions
+                dist.barrier(group=self.group)
             h = self.engine.peer_init(self.rank, self.world, cap)
-            ht = torch.from_numpy(h).to(dev)
-            hs = [torch.empty_like(ht) for _ in range(self.world)]
-            dist.all_gather(hs, ht, group=self.group)
-            self.engine.peer_open(torch.cat(hs).cpu().numpy())
+            hs = self._all_gather(torch.from_numpy(h).to(dev))
+            self.engine.peer_open(torch.cat([t.cpu() for t in hs]).numpy())
             self._peer_ready = True
+            self._peer_cap = cap
+            self.peer_inits = getattr(self, "peer_inits", 0) + 1
         m = self._meta_halo
         box = torch.tensor(self.box, dtype=torch.float32, device=dev)
         sh = torch.round((self.x_ext[self.n_home:] - self._xw[m[:, 0].long()]) / box) * box
@@ -440,8 +488,8 @@ class DomainDecomposition:
         ev = self._events() if self.profile_phases else None
         if prune is None:
             prune = bool(self.prune_every) and step % self.prune_every == 0
-        if self.halo == "p2p" and not (energy or virial):
-            return self._step_p2p(x_home, prune, ev)
+        if self.halo == "p2p":
+            return self._step_p2p(x_home, prune, ev, (1 if energy else 0) | (2 if virial else 0))
         if x_home is not None:
             self.x_ext[:self.n_home].copy_(x_home)
         if ev:
@@ -468,11 +516,7 @@ class DomainDecomposition:
             ev[3].record()
         res = None
         if flags:
-            e, v = eng.energies()
-            t = self.torch.tensor(np.concatenate([e, v]), dtype=self.torch.float64, device=self.device)
-            self.dist.all_reduce(t, group=self.group)
-            t = t.cpu().numpy()
-            res = (t[:2], t[2:].reshape(3, 3))
+            res = self._reduce_energies()
         eng.get_f(0, self.f_ext[:self.n_home])
         eng.get_f(1, self.f_ext[self.n_home:])
         self.halo_f()
@@ -482,14 +526,26 @@ class DomainDecomposition:
         f_home = self.f_ext[:self.n_home]
         return (f_home, res) if res is not None else f_home
 
-    def _step_p2p(self, x_home, prune, ev):
-        """Force-only step with the NVLink peer-memory halo: no messages, no pack/unpack, no
-        reverse pulses (csrc/peer.cu).  x_home=None: the coordinates of the last repartition
-        (or of the last NCCL-path step)."""
+    def _reduce_energies(self):
+        """This rank's (E, virial) share -> all-reduced totals (host arrays)."""
+        e, v = self.engine.energies()
+        t = self.torch.tensor(np.concatenate([e, v]), dtype=self.torch.float64, device=self.device)
+        t = self._all_reduce(t).cpu().numpy()
+        return t[:2], t[2:].reshape(3, 3)
+
+    def _step_p2p(self, x_home, prune, ev, flags=0):
+        """A step with the NVLink peer-memory halo: no messages, no pack/unpack, no reverse
+        pulses (csrc/peer.cu).  flags (1 energy, 2 virial): the nonlocal kernel accumulates
+        energies, and the virial's x (x) f is summed per grid before the forces move (halo
+        atoms before the push to their owners, home atoms before the inbox is added), so
+        energy / virial steps take the same halo as force-only ones.  x_home=None: the
+        coordinates of the last repartition (or of the last step)."""
         eng = self.engine
         self.seq += 1
         seq = self.seq & 0xFFFFFFFF
         x = self.x_ext[:self.n_home] if x_home is None else x_home.contiguous()
+        if flags:
+            eng.clear_energies()
         if ev:
             ev[0].record()
         eng.peer_put_x(x, seq)  # grid-0 X op + publish + signal
@@ -509,33 +565,35 @@ class DomainDecomposition:
                 eng.peer_halo_x(seq)
                 if prune:
                     eng.prune(1)
-                eng.peer_force_nonlocal(seq)
+                eng.peer_force_nonlocal(seq, flags)
                 self._ev_nl.record(self._side)
             if prune:
                 eng.prune(0)
-            eng.force(0, 0)
+            eng.force(0, flags)
             main.wait_event(self._ev_nl)
             f_home = self.f_ext[:self.n_home]
-            eng.peer_get_f(f_home, seq)  # wait for the senders, home forces + inbox
-            return f_home
-        if prune:
-            eng.prune(0)
-        eng.force(0, 0)
-        if ev:
-            ev[1].record()
-        eng.peer_halo_x(seq)  # wait for the owners, gather the halo over NVLink
-        if ev:
-            ev[2].record()
-        if prune:
-            eng.prune(1)
-        eng.peer_force_nonlocal(seq)  # j forces straight into the owners' inboxes
-        if ev:
-            ev[3].record()
-        f_home = self.f_ext[:self.n_home]
-        eng.peer_get_f(f_home, seq)  # wait for the senders, home forces + inbox
-        if ev:
-            ev[4].record()
-            self.phase_log.append(ev)
+            eng.peer_get_f(f_home, seq, flags)  # wait for the senders, home forces + inbox
+        else:
+            if prune:
+                eng.prune(0)
+            eng.force(0, flags)
+            if ev:
+                ev[1].record()
+            eng.peer_halo_x(seq)  # wait for the owners, gather the halo over NVLink
+            if ev:
+                ev[2].record()
+            if prune:
+                eng.prune(1)
+            eng.peer_force_nonlocal(seq, flags)  # j forces straight into the owners' inboxes
+            if ev:
+                ev[3].record()
+            f_home = self.f_ext[:self.n_home]
+            eng.peer_get_f(f_home, seq, flags)  # wait for the senders, home forces + inbox
+            if ev:
+                ev[4].record()
+                self.phase_log.append(ev)
+        if flags:
+            return f_home, self._reduce_energies()
         return f_home
 
     def _events(self):

@@ -117,8 +117,8 @@ def lib():
         L.nbx_peer_set_halo.argtypes = [vp, i32, vp, vp, vp, vp]
         L.nbx_peer_put_x.argtypes = [vp, vp, u32, vp]
         L.nbx_peer_halo_x.argtypes = [vp, u32, vp]
-        L.nbx_peer_force_nonlocal.argtypes = [vp, u32, vp]
-        L.nbx_peer_get_f.argtypes = [vp, vp, u32, vp]
+        L.nbx_peer_force_nonlocal.argtypes = [vp, u32, u32, vp]
+        L.nbx_peer_get_f.argtypes = [vp, vp, u32, u32, vp]
         L.nbx_peer_status.argtypes = [vp, vp]
         L.nbx_pme_create.argtypes = [C.c_int, vp, C.POINTER(vp)]
         L.nbx_pme_destroy.argtypes = [vp]

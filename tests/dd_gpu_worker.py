@@ -1,9 +1,22 @@
-"""torchrun worker for tests/test_dd_gpu.py: DD over NCCL on N GPUs vs the single-GPU engine.
+"""torchrun worker for tests/test_dd_gpu.py: DD on N ranks vs the single-GPU engine.
 
-    torchrun --nproc-per-node N --master-addr 127.0.0.1 tests/dd_gpu_worker.py <config> <natoms> <out.npz> [nccl|p2p]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 tests/dd_gpu_worker.py \
+        <config> <natoms|full> <out.npz> [nccl|p2p] [oversub]
 
-p2p: force-only steps go through the NVLink peer-memory halo (csrc/peer.cu) and are checked
-as well; energy/virial steps always take the NCCL path.
+Every rank runs the DD path of paper_2405_01420_b200.dd through libnbx.so.  Checked steps:
+  fa   force-only step after the first repartition;
+  f/e  energy + virial step on the same coordinates;
+  fb   force-only step with moved atoms and the rolling prune (halo coordinates refreshed);
+  fb2  a second force-only step (peer flags / inbox reuse);
+  f2/e2 energy + virial step on the moved coordinates;
+  f3/e3 energy + virial step after a second repartition from the moved coordinates.
+halo = p2p: every step, energy/virial ones included, goes through the NVLink peer-memory
+halo (csrc/peer.cu); halo = nccl: through the message-passing pulses.
+
+oversub: all N ranks share cuda:0 and talk over gloo (exchanges staged through host
+memory), and the peer-memory halo runs over CUDA IPC between processes on the same device.
+That is how a 1-GPU box executes dd.py and peer.cu end to end.  The single-GPU reference
+(rank 0, same device) is itself oracle-checked by tests/test_gpu_parity.py.
 """
 import os
 import sys
@@ -19,67 +32,84 @@ from paper_2405_01420_b200 import dd as DD  # noqa: E402
 from paper_2405_01420_b200 import nbx, systems  # noqa: E402
 
 
+def gather_home(d, t, world, dev, natoms):
+    """Rank-ordered home arrays -> [natoms, 3] in global-id order (on rank 0)."""
+    n = torch.tensor([d.n_home], dtype=torch.int64)
+    ns = d._all_gather(n.to(dev))
+    ns = [int(v) for v in ns]
+    mx = max(ns)
+    pad = lambda a: torch.cat([a, torch.zeros((mx - a.shape[0],) + a.shape[1:], dtype=a.dtype, device=a.device)])
+    gl = d._all_gather(pad(d.home_gid.contiguous()))
+    fl = d._all_gather(pad(t.contiguous()))
+    G = np.concatenate([gl[r][:ns[r]].cpu().numpy() for r in range(world)])
+    F = np.zeros((natoms, 3))
+    F[G] = np.concatenate([fl[r][:ns[r]].cpu().numpy() for r in range(world)])
+    return G, F
+
+
 def main():
-    cfg, natoms, out = sys.argv[1], int(sys.argv[2]), sys.argv[3]
+    cfg, natoms, out = sys.argv[1], sys.argv[2], sys.argv[3]
+    natoms = None if natoms == "full" else int(natoms)
     halo = sys.argv[4] if len(sys.argv) > 4 else "nccl"
+    oversub = len(sys.argv) > 5 and sys.argv[5] == "oversub"
     rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local)
+    devi = 0 if oversub else local
+    torch.cuda.set_device(devi)
+    dev = torch.device("cuda", devi)
+    if oversub:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=dev)
     s = systems.make(cfg, natoms)
-    d = DD.DomainDecomposition(s, rank, world, lambda sy, pbc: DD.NbxEngine(sy, local, pbc), device=dev,
+    d = DD.DomainDecomposition(s, rank, world, lambda sy, pbc: DD.NbxEngine(sy, devi, pbc), device=dev,
                                 halo=halo)
     xg = torch.from_numpy(s.x).to(dev)
     d.repartition(xg)
-    fa = d.step(None, step=1, prune=False).clone()  # force-only: the p2p path when halo=p2p
+    res = {}
+    res["fa"] = d.step(None, step=1, prune=False).clone()  # force-only
     f, (e, vir) = d.step(None, step=1, energy=True, virial=True, prune=False)
-    f = f.clone()  # step() returns a view of the rank's force buffer
-    # a second, non-search step with moved atoms (halo coordinates refreshed, prune on)
+    res["f"] = f.clone()  # step() returns a view of the rank's force buffer
+    # non-search steps with moved atoms (halo coordinates refreshed, prune on)
     rng = np.random.default_rng(3)
     disp = torch.from_numpy(rng.uniform(-0.01, 0.01, size=s.x.shape).astype(np.float32)).to(dev)
     x_home = d.x_ext[:d.n_home] + disp[d.home_gid.long()]
-    fb = d.step(x_home, step=10, prune=True).clone()
-    fb2 = d.step(x_home, step=11, prune=False).clone()  # a second step: inbox/flags reuse
+    res["fb"] = d.step(x_home, step=10, prune=True).clone()
+    res["fb2"] = d.step(x_home, step=11, prune=False).clone()  # a second step: inbox/flags reuse
     f2, (e2, vir2) = d.step(x_home, step=10, energy=True, virial=True, prune=True)
+    res["f2"] = f2.clone()
     torch.cuda.synchronize()
     d.check_peer()
-    gids = [torch.zeros(0)] * world
-    n = torch.tensor([d.n_home], device=dev)
-    ns = [torch.zeros_like(n) for _ in range(world)]
-    dist.all_gather(ns, n)
-    mx = int(max(int(v) for v in ns))
-    pad = lambda t, w: torch.cat([t, torch.zeros((mx - t.shape[0],) + t.shape[1:], dtype=t.dtype, device=dev)])
-    gl = [torch.zeros(mx, dtype=torch.int32, device=dev) for _ in range(world)]
-    fl = [torch.zeros((mx, 3), dtype=torch.float32, device=dev) for _ in range(world)]
-    fl2 = [torch.zeros((mx, 3), dtype=torch.float32, device=dev) for _ in range(world)]
-    dist.all_gather(gl, pad(d.home_gid, 1))
-    dist.all_gather(fl, pad(f.contiguous(), 1))
-    dist.all_gather(fl2, pad(f2.contiguous(), 1))
-    extra = {}
-    for name, t in (("fa", fa), ("fb", fb), ("fb2", fb2)):
-        lst = [torch.zeros((mx, 3), dtype=torch.float32, device=dev) for _ in range(world)]
-        dist.all_gather(lst, pad(t.contiguous(), 1))
-        extra[name] = lst
+    out_arrays = {}
+    for name, t in res.items():  # the first partition's home order
+        G, F = gather_home(d, t, world, dev, s.natoms)
+        out_arrays[name] = F
+        out_arrays["gids"] = G
+    # a second repartition from the moved coordinates (atoms change domains), then an energy step
+    x2 = xg + disp
+    d.repartition(x2)
+    f3, (e3, vir3) = d.step(None, step=100, energy=True, virial=True, prune=False)
+    torch.cuda.synchronize()
+    d.check_peer()
+    G3, F3 = gather_home(d, f3, world, dev, s.natoms)
+    out_arrays["f3"] = F3
+    out_arrays["gids3"] = G3
     if rank == 0:
-        G = np.concatenate([gl[r][:int(ns[r])].cpu().numpy() for r in range(world)])
-        F = np.zeros((s.natoms, 3))
-        F2 = np.zeros((s.natoms, 3))
-        F[G] = np.concatenate([fl[r][:int(ns[r])].cpu().numpy() for r in range(world)])
-        F2[G] = np.concatenate([fl2[r][:int(ns[r])].cpu().numpy() for r in range(world)])
-        FX = {}
-        for name, lst in extra.items():
-            FX[name] = np.zeros((s.natoms, 3))
-            FX[name][G] = np.concatenate([lst[r][:int(ns[r])].cpu().numpy() for r in range(world)])
-        # single-GPU reference with the same coordinates
-        nb = nbx.Nonbonded(s, device=local)
+        nb = nbx.Nonbonded(s, device=devi)
         nb.search(xg)
+        fa1 = nb.forces(xg)
         f1, (e1, v1) = nb.forces(xg, energy=True, virial=True)
-        x2 = xg + disp
         nb.put_x(x2)
         nb.prune()
+        fb1 = nb.forces(x2)
         f12, (e12, v12) = nb.forces(x2, energy=True, virial=True)
-        np.savez(out, gids=G, f=F, e=e, vir=vir, f_ref=f1.cpu().numpy(), e_ref=e1, vir_ref=v1, f2=F2, e2=e2,
-                 vir2=vir2, f2_ref=f12.cpu().numpy(), e2_ref=e12, vir2_ref=v12, natoms=s.natoms, **FX)
+        nb.search(x2)
+        f13, (e13, v13) = nb.forces(x2, energy=True, virial=True)
+        np.savez(out, e=e, vir=vir, e2=e2, vir2=vir2, e3=e3, vir3=vir3,
+                 fa_ref=fa1.cpu().numpy(), f_ref=f1.cpu().numpy(), e_ref=e1, vir_ref=v1,
+                 fb_ref=fb1.cpu().numpy(), f2_ref=f12.cpu().numpy(), e2_ref=e12, vir2_ref=v12,
+                 f3_ref=f13.cpu().numpy(), e3_ref=e13, vir3_ref=v13, natoms=s.natoms,
+                 peer_inits=getattr(d, "peer_inits", 0), n_home=d.n_home, n_ext=d.n_ext, **out_arrays)
+    dist.barrier()
     dist.destroy_process_group()
 
 

@@ -1,9 +1,18 @@
-"""Domain decomposition on real GPUs (NCCL), N = 2 / 4 / 8 as many as are visible.
+"""Domain decomposition on real GPUs: DD forces, energies and virial == the single-GPU engine
+(itself oracle-checked by tests/test_gpu_parity.py) on the same coordinates.
 
-DD forces, energies and virial == the single-GPU engine on the same coordinates, after a
-search step and after a moved-atoms prune step.  Skipped on a 1-GPU box (the host logic is
-covered on CPU by tests/test_dd.py)."""
+Two launch modes of the same worker (tests/dd_gpu_worker.py):
+  * one rank per GPU over NCCL (N = 2 / 4 / 8, skipped when fewer GPUs are visible), on the
+    BASELINE's decomposed configs at full size: STMV 1,066,628 atoms at N = 2/4/8 and the
+    12 M-atom water box at N = 8;
+  * oversubscribed: N ranks on cuda:0 over gloo (host-staged exchanges) with the peer-memory
+    halo over CUDA IPC on the same device -- so a 1-GPU box runs dd.py and csrc/peer.cu end to
+    end on the full-size STMV box and the 12 M box.
+Checked per case: force-only, energy + virial (both through the chosen halo), moved atoms with
+the rolling prune, and an energy step after a second repartition from moved coordinates
+(reference schedule: /root/reference/pkg/src/mdgpusim/pipeline.py:267-438)."""
 import os
+import socket
 import subprocess
 import sys
 import tempfile
@@ -23,31 +32,73 @@ def _ngpu():
     return torch.cuda.device_count()
 
 
-@pytest.mark.parametrize("halo", ["nccl", "p2p"])
-@pytest.mark.parametrize("world", [2, 4, 8])
-def test_dd_matches_single_gpu(gpu, world, halo):
-    """halo=p2p: force-only steps through the NVLink peer-memory halo (csrc/peer.cu)."""
-    if _ngpu() < world:
-        pytest.skip(f"needs {world} GPUs")
-    natoms = 150000 if world < 8 else 300000
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _run(world, config, natoms, halo, oversub=False, timeout=900):
     with tempfile.TemporaryDirectory() as tmp:
         out = os.path.join(tmp, "dd.npz")
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
-               "--master-addr", "127.0.0.1", "--master-port", str(29500 + world),
-               os.path.join(ROOT, "tests", "dd_gpu_worker.py"), "water12m", str(natoms), out, halo]
-        r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+               "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+               os.path.join(ROOT, "tests", "dd_gpu_worker.py"), config, str(natoms), out, halo]
+        if oversub:
+            cmd.append("oversub")
+        env = dict(os.environ, OMP_NUM_THREADS="2")
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, env=env)
         assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
-        d = np.load(out)
-    assert np.array_equal(np.sort(d["gids"]), np.arange(int(d["natoms"])))
+        return dict(np.load(out))
+
+
+def _check(d):
+    n = int(d["natoms"])
+    assert np.array_equal(np.sort(d["gids"]), np.arange(n))  # every atom has exactly one home
+    assert np.array_equal(np.sort(d["gids3"]), np.arange(n))
+    assert_forces(d["fa"], d["fa_ref"])
     assert_forces(d["f"], d["f_ref"])
     assert_energies(d["e"], d["e_ref"])
     assert_virial(d["vir"], d["vir_ref"])
+    assert_forces(d["fb"], d["fb_ref"])
+    assert_forces(d["fb2"], d["fb_ref"])
     assert_forces(d["f2"], d["f2_ref"])
     assert_energies(d["e2"], d["e2_ref"])
     assert_virial(d["vir2"], d["vir2_ref"])
-    assert_forces(d["fa"], d["f_ref"])
-    assert_forces(d["fb"], d["f2_ref"])
-    assert_forces(d["fb2"], d["f2_ref"])
+    assert_forces(d["f3"], d["f3_ref"])
+    assert_energies(d["e3"], d["e3_ref"])
+    assert_virial(d["vir3"], d["vir3_ref"])
+
+
+# ---- one GPU, N ranks sharing it (runs on the driver's 1-GPU box) ---------------------------
+@pytest.mark.parametrize("config,world,halo", [
+    ("stmv", 2, "p2p"),       # full STMV, 2x1x1, NVLink-form peer halo over same-device IPC
+    ("stmv", 2, "nccl"),      # full STMV, message halo (gloo, host-staged pulses)
+    ("stmv", 4, "p2p"),       # full STMV, 2x2x1
+    ("water12m", 8, "p2p"),   # full 12 M water, 2x2x2
+])
+def test_dd_oversubscribed_one_gpu(gpu, config, world, halo):
+    d = _run(world, config, "full", halo, oversub=True, timeout=1200)
+    _check(d)
+
+
+# ---- one rank per GPU over NCCL ---------------------------------------------------------------
+@pytest.mark.parametrize("halo", ["nccl", "p2p"])
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_dd_stmv_full_matches_single_gpu(gpu, world, halo):
+    """STMV-sized 1,066,628 atoms at N = 2/4/8 (BASELINE config 4), both halo forms."""
+    if _ngpu() < world:
+        pytest.skip(f"needs {world} GPUs")
+    _check(_run(world, "stmv", "full", halo))
+
+
+def test_dd_water12m_full_8gpu(gpu):
+    """12 M-atom water box at N = 8 (BASELINE config 5), peer-memory halo."""
+    if _ngpu() < 8:
+        pytest.skip("needs 8 GPUs")
+    _check(_run(8, "water12m", "full", "p2p", timeout=1500))
 
 
 @pytest.mark.parametrize("config", ["stmv_tab", "grappa1.5m", "rnase24k_lb"])
@@ -59,17 +110,4 @@ def test_dd_paper_flavours(gpu, world, config):
     if _ngpu() < world:
         pytest.skip(f"needs {world} GPUs")
     natoms = 60000 if config == "rnase24k_lb" else 150000
-    with tempfile.TemporaryDirectory() as tmp:
-        out = os.path.join(tmp, "dd.npz")
-        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
-               "--master-addr", "127.0.0.1", "--master-port", str(29520 + world),
-               os.path.join(ROOT, "tests", "dd_gpu_worker.py"), config, str(natoms), out, "p2p"]
-        r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
-        assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
-        d = np.load(out)
-    assert np.array_equal(np.sort(d["gids"]), np.arange(int(d["natoms"])))
-    assert_forces(d["f"], d["f_ref"])
-    assert_energies(d["e"], d["e_ref"])
-    assert_virial(d["vir"], d["vir_ref"])
-    assert_forces(d["fa"], d["f_ref"])
-    assert_forces(d["fb"], d["f2_ref"])
+    _check(_run(world, config, natoms, "p2p"))
