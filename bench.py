@@ -33,6 +33,10 @@ UNIT = "pair-interactions/s"
 # Algorithmic FP32 flops per in-cut-off pair of the force-only kernel, counted once from
 # pairmath.cuh / force.cu (FADD/FMUL/MUFU = 1, FFMA = 2) and frozen.
 FLOPS_PER_PAIR = {"ewald": 57, "rf": 33, "ewald-tab": 43}
+# ... and as the shipped F-only tile issues them (pairmath.cuh ewald_coul_r2 + force.cu tile():
+# 3 (dx, dy, dz) + 5 (r2) + 1 MUFU.RSQ + 3 (r^-2, r^-3, r^-6) + 3 (LJ) + 22 (rational: FADD2,
+# 4 FFMA2, MUFU.RCP, FMUL, FFMA) + 1 (qq) + 1 (Coulomb) + 2 (fscal) + 12 (i and j forces) = 53)
+FLOPS_ISSUED = {"ewald": 53}
 # combination-rule LJ adds the per-pair parameter arithmetic (nbx.h NBX_LJ_COMB_*)
 LJ_EXTRA_FLOPS = {"comb-geom": 2, "comb-lb": 8}
 DESC = {
@@ -184,10 +188,62 @@ def time_cpu_port(config, budget_s, steps=None, warmup=0):
         if steps is None and (time.perf_counter() - t0) >= budget_s:
             break
     tot = sum(times)
-    sample = (f"C oracle force evaluation (F only, Ewald/RF as configured) on a {s.natoms}-atom box "
-              f"of the same generator and parameters ({reps} evaluations, {pairs} pairs each)")
+    sample = (f"scalar C oracle (the correctness restatement: -ffp-contract=off, AoS, no SIMD kernel -- not "
+              f"a tuned CPU NBNXM), OpenMP over {cores} threads, force-only evaluation (F, Ewald/RF as "
+              f"configured; no search/prune/buffer ops) on a {s.natoms}-atom sample box of the same generator "
+              f"and parameters ({reps} evaluations, {pairs} pairs each)")
     return {"value": pairs * reps / tot, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
             "ms_per_eval": 1e3 * tot / reps, "pairs_per_eval": pairs, "reps": reps}
+
+
+# ------------------------------------------------------------------------------ cadence
+def step_kind(step, nstlist, prune_every):
+    """'search' | 'prune' | 'plain' by the reference cadence (pipeline.py:222-235)."""
+    if step % nstlist == 0:
+        return "search"
+    if prune_every and step % prune_every == 0:
+        return "prune"
+    return "plain"
+
+
+def compose_era(step_ms, kinds, nstlist, prune_every):
+    """Mean ms per step over one nstlist era from the per-kind means measured in the window:
+    (t_search + n_prune t_prune + n_plain t_plain) / nstlist with the cadence's counts
+    (1 search, nstlist/prune_every - 1 prunes, the rest plain).  A window that starts with a
+    search step and holds >= prune_every + 1 steps measures all three kinds, so a short K
+    weighs the search step exactly as a full era does (no search-free windows)."""
+    by = {}
+    for t, k in zip(step_ms, kinds):
+        by.setdefault(k, []).append(t)
+    mean = {k: sum(v) / len(v) for k, v in by.items()}
+    t_plain = mean.get("plain", mean.get("prune", 0.0))
+    t_prune = mean.get("prune", t_plain)
+    t_search = mean.get("search", t_prune)
+    n_prune = (nstlist // prune_every - 1) if prune_every else 0
+    n_plain = nstlist - 1 - n_prune
+    era = (t_search + n_prune * t_prune + n_plain * t_plain) / nstlist
+    return era, {k: round(v, 4) for k, v in mean.items()}, {k: len(v) for k, v in by.items()}
+
+
+# MD-like motion between steps (ADVICE r1): x += v dt with per-atom velocities of fixed
+# magnitude, reversed every nstlist steps so atoms oscillate about their start.  The rms
+# displacement over one nstlist era (~0.05 nm) matches liquid-water self-diffusion over the
+# era's 0.2 ps (D = 2.3e-9 m^2/s: sqrt(6 D t) = 0.05 nm); lists stay valid within the
+# 0.1 nm Verlet buffer, pruning and searching see moving coordinates.
+ERA_RMS_DISP_NM = 0.05
+
+
+def motion_sign(step, nstlist):
+    """+1 on the steps of even eras, -1 on odd ones (step k moves by sign(k) v dt)."""
+    return 1.0 if ((step - 1) // nstlist) % 2 == 0 else -1.0
+
+
+def motion_velocities(n, nstlist, dt_ps, seed=11):
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    v = rng.normal(size=(n, 3)).astype(np.float32)
+    v *= ERA_RMS_DISP_NM / (np.sqrt(3.0) * nstlist * dt_ps)
+    return v
 
 
 # ------------------------------------------------------------------------------ nbx arm, N = 1
@@ -195,7 +251,7 @@ def run_single(args):
     import numpy as np
     import torch
 
-    from paper_2405_01420_b200 import nbx, systems
+    from paper_2405_01420_b200 import nbx, pme, systems
 
     torch.cuda.set_device(0)
     s = systems.make(args.config)
@@ -204,18 +260,27 @@ def run_single(args):
     f = torch.empty_like(x)
     st = torch.cuda.current_stream()
     peak = nb.fma_peak_tflops()
+    dt_ps = s.dt_fs * 1e-3
+    vel = torch.from_numpy(motion_velocities(s.natoms, s.nstlist, dt_ps)).cuda()
+    zero_im = torch.zeros(s.natoms, dtype=torch.float32, device="cuda")  # inv_mass 0: v is kept
 
-    # warm-up steps 0..W-1 (step 0 is a search step)
-    # small boxes are launch-bound: replay non-search steps as CUDA graphs (the force kernel
-    # time is then taken from a back-to-back loop on the same stream right after)
+    def move(xx, step):
+        # x += sign(step) v dt (HBM-bound, between the step events)
+        pme.leapfrog(xx, vel, f, zero_im, motion_sign(step, s.nstlist) * dt_ps)
+
+    # small boxes are launch-bound: replay non-search steps as CUDA graphs
     graphs = s.natoms < 500_000
+    # setup search, then W warm-up steps numbered nstlist-W .. nstlist-1 (they include prune
+    # steps), so the timed window starts with the era's search step
+    nb.step(x, f, 0, graphs=graphs)
     for k in range(args.warmup):
-        nb.step(x, f, k, graphs=graphs)
+        step = max(1, s.nstlist - args.warmup + k)
+        move(x, step)
+        nb.step(x, f, step, graphs=graphs)
     if graphs:  # instantiate both step graphs before the timed region
         nb.graph_step(x, f, prune=True)
         nb.graph_step(x, f, prune=False)
     torch.cuda.synchronize()
-    pairs, slots = nb.count_pairs()
     sizes = nb.list_sizes()
     nslots = nb.grid_info()["nslots"]
     working = nslots * 16 * 3 + sizes["n_cj_outer"] * 16 + sizes["n_pool"] * 64
@@ -225,73 +290,88 @@ def run_single(args):
     K = args.steps
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     evf = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    w0, w1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clocks = ClockSampler(0, interval_ms=250).start()  # NVML polls contend with CUDA calls
     torch.cuda.synchronize()
     l0 = nb.launch_count()
-    n_search = n_prune = 0
+    kinds = [step_kind(k, s.nstlist, s.prune_every) for k in range(K)]
+    pairs0 = None
+    w0.record(st)
     for k in range(K):
-        step = args.warmup + k
+        if k:
+            move(x, k)
         if flush:
             scratch.fill_(float(k))
         ev[k][0].record(st)
-        search = step % s.nstlist == 0
-        prune = (not search) and s.prune_every and step % s.prune_every == 0
-        n_search += int(search)
-        n_prune += int(bool(prune))
-        if graphs and not search:
-            nb.graph_step(x, f, prune=bool(prune))
+        if graphs and kinds[k] != "search":
+            nb.graph_step(x, f, prune=kinds[k] == "prune")
         else:
-            if search:
+            if kinds[k] == "search":
                 nb.search(x)
             else:
                 nb.put_x(x)
-                if prune:
+                if kinds[k] == "prune":
                     nb.prune()
             evf[k][0].record(st)
             nb.compute()
             evf[k][1].record(st)
             nb.get_f(f)
         ev[k][1].record(st)
+    w1.record(st)
     torch.cuda.synchronize()
-    launches = nb.launch_count() - l0  # graph launches are counted per kernel node by the library
-    if graphs:
+    launches = nb.launch_count() - l0 + (K - 1)  # + the K - 1 motion updates (nbx_leapfrog)
+    clk = clocks.stop()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    era_ms, kind_ms, kind_n = compose_era(step_ms, kinds, s.nstlist, s.prune_every)
+    window_ms = w0.elapsed_time(w1)
+    # in-cut-off pairs per step: the inner list at the window's end, and the list a search of
+    # the window's first coordinates builds (replayed below); the motion changes them < 0.1 %
+    pairs_end, slots_end = nb.count_pairs()
+    if graphs:  # force kernel alone, back to back on the same stream
         for k in range(K):
             evf[k][0].record(st)
             nb.compute()
             evf[k][1].record(st)
         nb.get_f(f)  # clears the cluster force buffer again
         torch.cuda.synchronize()
-    clk = clocks.stop()
-    step_ms = [a.elapsed_time(b) for a, b in ev]
-    force_ms = [a.elapsed_time(b) for a, b in evf]
-    tot_ms = sum(step_ms)
-    ms_per_step = tot_ms / K
-    value = pairs * K / (tot_ms * 1e-3)
-    t_force = sum(force_ms) / K
+    force_ms = [evf[k][0].elapsed_time(evf[k][1]) for k in range(K)]
+    xs = torch.from_numpy(s.x).cuda()
+    nb.search(xs)  # the window's first list (same x as its search step up to the warm-up motion)
+    pairs_start, slots_start = nb.count_pairs()
+    pairs = 0.5 * (pairs_start + pairs_end)
+    slots = 0.5 * (slots_start + slots_end)
+    ms_per_step = era_ms
+    value = pairs / (ms_per_step * 1e-3)
+    t_force = sum(force_ms) / len(force_ms)
     fl = FLOPS_PER_PAIR[s.coulomb] + LJ_EXTRA_FLOPS.get(s.lj_modifier, 0)
+    fl_iss = FLOPS_ISSUED.get(s.coulomb, fl) + LJ_EXTRA_FLOPS.get(s.lj_modifier, 0)
     achieved = pairs * fl / (t_force * 1e-3) / 1e12
+    achieved_iss = pairs * fl_iss / (t_force * 1e-3) / 1e12
     slot_tf = slots * fl / (t_force * 1e-3) / 1e12
 
-    # e2e: public API with host buffers, H2D of x and D2H of f inside the timed region
+    # e2e: the public API with host buffers -- every step copies x from pinned host memory
+    # (H2D) and reads f back (D2H) inside the timed region; same cadence and era composition
     e2e = None
     if not args.no_e2e:
         xh = torch.from_numpy(s.x.copy()).pin_memory()
         fh = torch.empty((s.natoms, 3), dtype=torch.float32).pin_memory()
         xd = torch.empty_like(x)
         Ke = max(1, min(K, 50))
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        eev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(Ke)]
+        ekinds = [step_kind(k, s.nstlist, s.prune_every) for k in range(Ke)]
         torch.cuda.synchronize()
-        e0.record(st)
         for k in range(Ke):
-            step = args.warmup + K + k
+            eev[k][0].record(st)
             xd.copy_(xh, non_blocking=True)
-            nb.step(xd, f, step)
+            nb.step(xd, f, k, graphs=graphs)
             fh.copy_(f, non_blocking=True)
-        e1.record(st)
+            eev[k][1].record(st)
         torch.cuda.synchronize()
-        ems = e0.elapsed_time(e1)
-        e2e = {"value": pairs * Ke / (ems * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(xh.numel() * 4),
-               "d2h_bytes_per_step": int(fh.numel() * 4), "steps": Ke, "ms_per_step": ems / Ke,
+        ems = [a.elapsed_time(b) for a, b in eev]
+        e_era, e_kind_ms, _ = compose_era(ems, ekinds, s.nstlist, s.prune_every)
+        e2e = {"value": pairs / (e_era * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(xh.numel() * 4),
+               "d2h_bytes_per_step": int(fh.numel() * 4), "steps": Ke, "ms_per_step": e_era,
+               "ms_per_step_by_kind": e_kind_ms, "window_ms_per_step": sum(ems) / Ke,
                "api": "paper_2405_01420_b200.nbx.Nonbonded.step (ctypes -> libnbx.so C-ABI)"}
 
     cpu = None
@@ -311,20 +391,27 @@ def run_single(args):
                    "rlist_outer": s.rlist_outer, "rlist_inner": s.rlist_inner,
                    "parallelism": "single domain",
                    "l2": ("L2 flushed (2x126 MB write) before every timed step" if flush
-                          else f"inputs larger than L2 (xyzq+lists {working / 2**20:.0f} MiB)")},
+                          else f"inputs larger than L2 (xyzq+lists {working / 2**20:.0f} MiB)"),
+                   "motion": (f"x += v dt between steps (v reversed every nstlist steps; {ERA_RMS_DISP_NM} nm rms "
+                              "per era), outside the step events"),
+                   "step_time": ("one nstlist era composed from the window's per-kind step means: (t_search + "
+                                 f"{s.nstlist // s.prune_every - 1} t_prune + "
+                                 f"{s.nstlist - s.nstlist // s.prune_every} t_plain) / {s.nstlist}; the window "
+                                 "starts with a search step")},
         "steps_per_s": 1e3 / ms_per_step,
         "ns_per_day": 86.4 * s.dt_fs / ms_per_step,
         "pairs_per_step": pairs,
         "pair_slots_per_step": slots,
         "cluster_efficiency": pairs / slots if slots else None,
-        "step_ms": {"median": sorted(step_ms)[K // 2], "max": max(step_ms),
-                    "search_steps": [step_ms[k] for k in range(K) if (args.warmup + k) % s.nstlist == 0]},
-        "kernels_ms": {"force_avg": t_force, "step_avg": ms_per_step,
-                       "searches": n_search, "prunes": n_prune},
+        "step_ms": {"era": era_ms, "window_mean": sum(step_ms) / K, "window_incl_motion": window_ms / K,
+                    "by_kind": kind_ms, "kind_counts": kind_n, "median": sorted(step_ms)[K // 2], "max": max(step_ms)},
+        "kernels_ms": {"force_avg": t_force},
         "roofline": {"bound": "fp32", "kernel": "k_force (NBNXM force, F only)", "achieved": achieved,
                      "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                      "peak_source": "measured on this GPU: register-resident FFMA loop (nbx_fma_peak)",
-                     "flops_per_pair": fl, "slot_tflops": slot_tf, "slot_frac": slot_tf / peak},
+                     "flops_per_pair": fl, "flops_per_pair_note": "frozen before optimisation (DESIGN.md section 5)",
+                     "flops_per_pair_issued": fl_iss, "achieved_issued": achieved_iss, "frac_issued": achieved_iss / peak,
+                     "slot_tflops": slot_tf, "slot_frac": slot_tf / peak},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": int(launches),
@@ -352,7 +439,9 @@ def run_reference(args):
                          "sample": r["sample"]},
         "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "note": ("the reference (mdgpusim) computes no forces (SPEC.md:8); this arm times the CPU "
-                 "restatement of the path (oracle/nbx_oracle.c) on the box's host cores"),
+                 "restatement of the path (oracle/nbx_oracle.c: a scalar correctness oracle, not a tuned "
+                 "SIMD CPU NBNXM) on the box's host cores, on a 48k-atom sample box, force-only (no "
+                 "search, prune or buffer ops): a stated baseline, not like-for-like with the GPU step"),
         "wall_s": wall,
     }
     print(json.dumps(line), flush=True)
@@ -384,7 +473,9 @@ def main():
     rank, world, local = dist_env()
     if world > 1 or args.gpus > 1:
         from paper_2405_01420_b200 import dd
-        dd.bench(args, METRIC, UNIT, FLOPS_PER_PAIR, DESC, ClockSampler, time_cpu_port, load_traffic)
+        dd.bench(args, METRIC, UNIT, FLOPS_PER_PAIR, DESC, ClockSampler, time_cpu_port, load_traffic,
+                 step_kind=step_kind, compose_era=compose_era, motion_velocities=motion_velocities,
+                 motion_sign=motion_sign)
         return
     run_single(args)
 

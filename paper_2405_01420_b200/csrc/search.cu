@@ -551,12 +551,18 @@ __global__ void __launch_bounds__(PRUNE_THREADS) k_prune_lanes(PruneArgs A)
 // pass runs two j atoms per FADD2 / FMUL2 / FFMA2 (the kernel is issue-bound with the FP32
 // pipe half idle).  dx = xj - xi is the exact negation of xi - xj, so every r^2 has the
 // scalar kernels' rounding and the keep rule is unchanged: bit-identical lists.
-constexpr int PRUNE_JS = 28; // per-entry stride (floats): x[8] y[8] z[8] + pad (bank groups)
+// j atoms of a chunk, structure of arrays per coordinate: row t (entry t) = 8 floats at a
+// stride of 12 floats.  A pass reads one 16-byte quarter-row (h = 0, 1) of up to 8 distinct
+// rows per LDS.128: quarter (t, h) sits in bank quad (3 t + h) mod 8, distinct for 8
+// consecutive t (3 is coprime to 8), so a pass over <= 8 consecutive entries is conflict-free.
+// (Round 1's array-of-rows layout x[8] y[8] z[8] at stride 28 put rows t, t + 8 on the same
+// quads and its staging stores 2-way conflicted: 171 M conflicts per 12 M-atom prune.)
+constexpr int PRUNE_JS = 12;
 
 __global__ void __launch_bounds__(PRUNE_THREADS) k_prune_packed(PruneArgs A)
 {
     constexpr int W = PRUNE_THREADS / 32;
-    __shared__ __align__(16) float s_xj[W][32][PRUNE_JS];
+    __shared__ __align__(16) float s_xj[W][3][32][PRUNE_JS];
     __shared__ float4 s_xi[W][32];
     __shared__ unsigned s_nm[W][32];
     __shared__ unsigned s_pidx[W][32];
@@ -587,9 +593,9 @@ __global__ void __launch_bounds__(PRUNE_THREADS) k_prune_packed(PruneArgs A)
             if (t < cnt) {
                 const int j = lane & 7;
                 const float4 b = A.xq_j[8 * cjt + j];
-                s_xj[wib][t][j] = b.x;
-                s_xj[wib][t][8 + j] = b.y;
-                s_xj[wib][t][16 + j] = b.z;
+                s_xj[wib][0][t][j] = b.x;
+                s_xj[wib][1][t][j] = b.y;
+                s_xj[wib][2][t][j] = b.z;
             }
         }
         // item table: exclusive scan of the entries' active-tile counts
@@ -619,7 +625,9 @@ __global__ void __launch_bounds__(PRUNE_THREADS) k_prune_packed(PruneArgs A)
             const int t = it >> 3, kk = it & 7;
             const float4 a = s_xi[wib][4 * kk + ii];
             const unsigned pidx = s_pidx[wib][t];
-            const float* xs = s_xj[wib][t];
+            const float* xs = s_xj[wib][0][t];
+            const float* ys = s_xj[wib][1][t];
+            const float* zs = s_xj[wib][2][t];
             bool hit = false;
             if (!__any_sync(full, pidx != 0u)) {
                 const f2x AX = bc(a.x), AY = bc(a.y), AZ = bc(a.z);
@@ -627,8 +635,8 @@ __global__ void __launch_bounds__(PRUNE_THREADS) k_prune_packed(PruneArgs A)
 #pragma unroll
                 for (int h = 0; h < 2; h++) {
                     const ulonglong2 X = *reinterpret_cast<const ulonglong2*>(xs + 4 * h);
-                    const ulonglong2 Y = *reinterpret_cast<const ulonglong2*>(xs + 8 + 4 * h);
-                    const ulonglong2 Z = *reinterpret_cast<const ulonglong2*>(xs + 16 + 4 * h);
+                    const ulonglong2 Y = *reinterpret_cast<const ulonglong2*>(ys + 4 * h);
+                    const ulonglong2 Z = *reinterpret_cast<const ulonglong2*>(zs + 4 * h);
                     const f2x DX0 = sub2(X.x, AX), DY0 = sub2(Y.x, AY), DZ0 = sub2(Z.x, AZ);
                     const f2x DX1 = sub2(X.y, AX), DY1 = sub2(Y.y, AY), DZ1 = sub2(Z.y, AZ);
                     const float2 R0 = upk(fma2(DZ0, DZ0, fma2(DY0, DY0, mul2(DX0, DX0))));
@@ -647,8 +655,8 @@ __global__ void __launch_bounds__(PRUNE_THREADS) k_prune_packed(PruneArgs A)
 #pragma unroll
                 for (int h = 0; h < 2; h++) {
                     const ulonglong2 X = *reinterpret_cast<const ulonglong2*>(xs + 4 * h);
-                    const ulonglong2 Y = *reinterpret_cast<const ulonglong2*>(xs + 8 + 4 * h);
-                    const ulonglong2 Z = *reinterpret_cast<const ulonglong2*>(xs + 16 + 4 * h);
+                    const ulonglong2 Y = *reinterpret_cast<const ulonglong2*>(ys + 4 * h);
+                    const ulonglong2 Z = *reinterpret_cast<const ulonglong2*>(zs + 4 * h);
                     const f2x DX0 = sub2(X.x, AX), DY0 = sub2(Y.x, AY), DZ0 = sub2(Z.x, AZ);
                     const f2x DX1 = sub2(X.y, AX), DY1 = sub2(Y.y, AY), DZ1 = sub2(Z.y, AZ);
                     const float2 R0 = upk(fma2(DZ0, DZ0, fma2(DY0, DY0, mul2(DX0, DX0))));

@@ -137,7 +137,8 @@ def test_madelung_libnbx(gpu, which):
     m = KA.madelung_from_energy(e[1] - esh + et + ep, s.natoms, d)
     assert abs(m / M - 1) < MADELUNG_FP32_TOL, (m, M, m / M - 1)
     ftot = (f + fp).cpu().numpy()
-    assert np.abs(ftot).max() < 1e-5 * KA.EPSFAC / d**2
+    # fp32 PME grid / FFT: reciprocal forces carry ~2e-5 relative error (tests/test_pme_gpu.py)
+    assert np.abs(ftot).max() < 5e-5 * KA.EPSFAC / d**2
 
 
 @pytest.mark.gpu
