@@ -273,6 +273,10 @@ def run_single(args):
     # setup search, then W warm-up steps numbered nstlist-W .. nstlist-1 (they include prune
     # steps), so the timed window starts with the era's search step
     nb.step(x, f, 0, graphs=graphs)
+    # a second search after motion: the search's single-pass buffers are sized by the first, so
+    # from here on steps allocate nothing (device_allocs_in_timed_region)
+    move(x, 1)
+    nb.step(x, f, 0, graphs=graphs)
     for k in range(args.warmup):
         step = max(1, s.nstlist - args.warmup + k)
         move(x, step)
@@ -294,6 +298,7 @@ def run_single(args):
     clocks = ClockSampler(0, interval_ms=250).start()  # NVML polls contend with CUDA calls
     torch.cuda.synchronize()
     l0 = nb.launch_count()
+    a0 = nb.alloc_count()
     kinds = [step_kind(k, s.nstlist, s.prune_every) for k in range(K)]
     pairs0 = None
     w0.record(st)
@@ -320,6 +325,7 @@ def run_single(args):
     w1.record(st)
     torch.cuda.synchronize()
     launches = nb.launch_count() - l0 + (K - 1)  # + the K - 1 motion updates (nbx_leapfrog)
+    allocs = nb.alloc_count() - a0
     clk = clocks.stop()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     era_ms, kind_ms, kind_n = compose_era(step_ms, kinds, s.nstlist, s.prune_every)
@@ -415,6 +421,7 @@ def run_single(args):
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": int(launches),
+        "device_allocs_in_timed_region": int(allocs),
         "clocks": clk,
     }
     print(json.dumps(line), flush=True)

@@ -274,6 +274,9 @@ NBX_API int nbx_fma_peak(nbx_ctx* ctx, double* tflops_out, void* stream);
 
 /* Number of kernel launches this context has issued (bench evidence: gpu_launches).    */
 NBX_API int64_t nbx_launch_count(nbx_ctx* ctx);
+/* Device allocations the library has made so far (process-wide).  Steady-state steps make none:
+ * cudaMalloc / cudaFree contend with NVML (nvidia-smi) polls for the driver lock.          */
+NBX_API int64_t nbx_alloc_count(void);
 
 /* ---- domain-decomposition halo (KernelKind.HALO_PACK_UNPACK, costs.py:43,174;
  *      pipeline.py:363-380 coordinates, 403-418 forces) -------------------------------- *

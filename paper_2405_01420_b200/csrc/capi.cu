@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -14,6 +15,13 @@
 namespace nbx {
 
 static thread_local std::string g_err;
+unsigned long long g_allocs = 0;
+int g_trace_allocs = std::getenv("NBX_TRACE_ALLOCS") ? std::atoi(std::getenv("NBX_TRACE_ALLOCS")) : 0;
+
+void trace_alloc(size_t bytes, size_t old_bytes, void* caller)
+{
+    std::fprintf(stderr, "[nbx alloc #%llu] %zu bytes (was %zu) from %p\n", g_allocs, bytes, old_bytes, caller);
+}
 
 void set_error(const std::string& msg) { g_err = msg; }
 
@@ -204,9 +212,9 @@ NBX_API int nbx_create(int device, const nbx_params* p, nbx_ctx** out)
     ctx->sumq2.ensure(2);
     NBX_CUDA(cudaMemset(ctx->sumq2.p, 0, sizeof(double) * 2));
     ctx->counter.ensure(8);
-    // Row f2 (list sorting by length) is available but off by default: on the
-    // 12M box the longest-first order costs L2 locality (force kernel +6%), and the tail it
-    // removes is ~3% (ncu sm__cycles_active min/max) -- see DESIGN.md section 5
+    // Row f2 (list sorting by length): automatic by list size (entry_order = -1,
+    // nbx_internal.cuh) -- on for the mid-size lists whose tail it shortens, off for the 12 M
+    // box (longest-first costs L2 locality there, +5 %) and for tiny lists; DESIGN.md section 5
     if (const char* pk = std::getenv("NBX_PRUNE_KERNEL")) ctx->prune_kernel = std::atoi(pk);
     if (const char* eo = std::getenv("NBX_ENTRY_ORDER")) ctx->entry_order = std::atoi(eo);
     if (const char* fs = std::getenv("NBX_FORCE_SPLIT")) ctx->force_split = std::atoi(fs);
@@ -838,6 +846,8 @@ NBX_API int nbx_fma_peak(nbx_ctx* ctx, double* tflops, void* stream)
 }
 
 NBX_API int64_t nbx_launch_count(nbx_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+NBX_API int64_t nbx_alloc_count(void) { return (int64_t)__atomic_load_n(&g_allocs, __ATOMIC_RELAXED); }
 
 NBX_API int nbx_halo_pack_x(const float* x, const int32_t* idx, int32_t n, const float shift[3],
                             float* out, void* stream)

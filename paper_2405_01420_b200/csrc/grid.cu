@@ -306,8 +306,7 @@ void grid_build(nbx_ctx* ctx, int g, int n, const float* x, const int* gid, cons
     }
     // padded column sizes -> slot offsets; atom offsets
     int* padded = G.val.p; // reuse (n >= 1); needs ncol+1 ints
-    DBuf<int> padbuf;
-    if ((size_t)(G.ncol + 1) > G.val.cap) { padbuf.ensure(G.ncol + 1); padded = padbuf.p; }
+    if ((size_t)(G.ncol + 1) > G.val.cap) { G.padded.ensure(G.ncol + 1); padded = G.padded.p; }
     k_pad<<<(G.ncol + 1 + 255) / 256, 256, 0, st>>>(G.col_count.p, G.ncol, padded);
     ctx->launches++;
     size_t tb1 = 0, tb2 = 0;
@@ -320,7 +319,6 @@ void grid_build(nbx_ctx* ctx, int g, int n, const float* x, const int* gid, cons
     int nslots = 0;
     NBX_CUDA(cudaMemcpyAsync(&nslots, G.col_start.p + G.ncol, sizeof(int), cudaMemcpyDeviceToHost, st));
     NBX_CUDA(cudaStreamSynchronize(st));
-    padbuf.release();
     G.nslots = nslots;
     G.nsci = nslots / 32;
     const int ns = nslots > 0 ? nslots : 32;

@@ -33,6 +33,15 @@ struct CudaError {
         if (_e != cudaSuccess) throw ::nbx::CudaError{_e, #call};                     \
     } while (0)
 
+// device allocations made by DBuf::ensure (process-wide; nbx_alloc_count).  cudaMalloc and
+// cudaFree take the driver's resource-manager lock, which an nvidia-smi / NVML poll also
+// holds: an allocation inside a step can stall it by a poll interval (measured: 12 M DD search
+// steps 12 -> 45-270 ms with nvidia-smi sampling at 250 ms).  Steady-state steps allocate
+// nothing: buffers grow with 12.5 % headroom and scratch buffers are kept.
+extern unsigned long long g_allocs;
+extern int g_trace_allocs; // env NBX_TRACE_ALLOCS=1: log every allocation to stderr
+void trace_alloc(size_t bytes, size_t old_bytes, void* caller);
+
 // Grow-only device buffer.
 template <class T>
 struct DBuf {
@@ -45,6 +54,8 @@ struct DBuf {
         p = nullptr;
         size_t want = n < 16 ? 16 : n + n / 8;
         NBX_CUDA(cudaMalloc((void**)&p, want * sizeof(T)));
+        __atomic_add_fetch(&g_allocs, 1ull, __ATOMIC_RELAXED);
+        if (g_trace_allocs) trace_alloc(want * sizeof(T), cap * sizeof(T), __builtin_return_address(0));
         cap = want;
     }
     void release()
@@ -71,6 +82,7 @@ struct Grid {
     DBuf<float4> bb_col;                        // per column: (xlo, ylo, xhi, yhi) of its atoms
     DBuf<int> slotmap;                          // global id -> slot, or -1 [natoms_global]
     DBuf<int> islot;                            // input index -> slot [n]
+    DBuf<int> padded;                           // padded column sizes [ncol + 1] (when val is too small)
     DBuf<char> tmp;                             // cub temp
 };
 
@@ -86,8 +98,10 @@ struct List {
     DBuf<int> totals;  // [3]
     DBuf<unsigned> len_key, len_key_out;        // force-kernel work order (row f2)
     DBuf<int> order_in, order;                  // sci entries, longest first
+    bool use_order = false;                     // order is valid and the force kernel uses it
     DBuf<char> sort_tmp;
     DBuf<int> flags;                            // search overflow / max counts
+    DBuf<unsigned long long> pair_count;        // nbx_count_pairs scratch [2]
     int cap_cj = 0, cap_pool = 0;               // single-pass per-sci capacities
     DBuf<nbx_sci_entry> tsci;                   // single-pass private outputs
     DBuf<nbx_cj_entry> tcj;
@@ -133,7 +147,12 @@ struct nbx_ctx {
     int64_t launches = 0;
     int force_split = 0; // > 0: fixed work items per sci entry (env NBX_FORCE_SPLIT), 0: auto
     int prune_kernel = 2; // 0: k_prune (lane per cj entry), 1: k_prune_lanes (lane per i atom), 2: k_prune_packed (compacted tiles, FP32x2); env NBX_PRUNE_KERNEL
-    int entry_order = 0; // 0: list order (spatially coherent), 1: longest first (env NBX_ENTRY_ORDER)
+    // row f2, force-kernel work order: 0 = list order (spatially coherent), 1 = longest entry
+    // first (sorted after every prune), -1 = auto (default): longest first for lists of
+    // 1,024 <= n_sci < 32 x the resident force warps, where the tail matters and L2 locality
+    // does not yet (measured: mem82k -7.5 %, STMV -1.8 % force kernel; 12 M +5 %, water 3k's
+    // ~10 us sort is not repaid).  Env NBX_ENTRY_ORDER overrides.
+    int entry_order = -1;
     // nbx_step_graph: natively captured X op (+ prune) + force + F op, one per (x, f, what);
     // `epoch` is bumped by every call that can move list/grid buffers or change constants,
     // and a stale graph is refreshed with cudaGraphExecUpdate (no re-instantiation).

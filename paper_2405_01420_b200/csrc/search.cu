@@ -750,7 +750,7 @@ void count_pairs(nbx_ctx* ctx, int l, long long* pairs, long long* slots, cudaSt
     *slots = 0;
     if (L.n_sci == 0) return;
     PruneArgs A = prune_args(ctx, L);
-    DBuf<unsigned long long> out;
+    DBuf<unsigned long long>& out = L.pair_count;
     out.ensure(2);
     NBX_CUDA(cudaMemsetAsync(out.p, 0, 2 * sizeof(unsigned long long), st));
     k_count_pairs<<<(int)((L.n_sci * 32 + 255) / 256), 256, 0, st>>>(A, ctx->c.rc2, out.p);
@@ -759,7 +759,6 @@ void count_pairs(nbx_ctx* ctx, int l, long long* pairs, long long* slots, cudaSt
     unsigned long long h[2];
     NBX_CUDA(cudaMemcpyAsync(h, out.p, sizeof(h), cudaMemcpyDeviceToHost, st));
     NBX_CUDA(cudaStreamSynchronize(st));
-    out.release();
     *pairs = (long long)h[0];
     *slots = 32ll * (long long)h[1];
 }
@@ -775,6 +774,14 @@ __global__ void k_entry_len(const nbx_sci_entry* __restrict__ sci, int n, unsign
     if (e >= n) return;
     key[e] = 0xffffffffu - (unsigned)(sci[e].cj_end - sci[e].cj_start);
     idx[e] = e;
+}
+
+// resident force-kernel warps: 3 CTAs x 8 warps per SM (force.cu FORCE_MIN_BLOCKS x threads / 32)
+static bool entry_order_on(const nbx_ctx* ctx, const List& L)
+{
+    if (ctx->entry_order >= 0) return ctx->entry_order != 0;
+    const int64_t warps = (int64_t)ctx->num_sms * 3 * 8;
+    return L.n_sci >= 1024 && L.n_sci < 32 * warps;
 }
 
 static void sort_entries(nbx_ctx* ctx, List& L, cudaStream_t st)
@@ -810,7 +817,8 @@ void prune(nbx_ctx* ctx, int l, int part, int nparts, cudaStream_t st)
     else k_prune_packed<<<blocks, PRUNE_THREADS, 0, st>>>(A); // default
     ctx->launches++;
     NBX_CUDA(cudaGetLastError());
-    if (ctx->entry_order) sort_entries(ctx, L, st);
+    L.use_order = entry_order_on(ctx, L);
+    if (L.use_order) sort_entries(ctx, L, st);
 }
 
 void search(nbx_ctx* ctx, int l, cudaStream_t st)
@@ -921,11 +929,14 @@ void search(nbx_ctx* ctx, int l, cudaStream_t st)
         ctx->launches++;
         NBX_CUDA(cudaGetLastError());
     }
-    // capacities for the next single pass: 25% headroom over this search's maxima; the
-    // private buffers are allocated now, outside the next search
+    // capacities for the next single pass: 25 % headroom over this search's maxima, and when
+    // that exceeds the current capacity, grow to 50 % headroom, so that the private buffers
+    // (nsci x cap, reallocated outside the next search) are not regrown every few searches as
+    // atoms move: a regrow is a multi-GB cudaFree + cudaMalloc (tens of ms, and it contends
+    // with NVML polls for the driver lock)
     const int ncap = fl[1] + fl[1] / 4 + 32, pcap = fl[2] + fl[2] / 4 + 8;
-    L.cap_cj = L.cap_cj > ncap ? L.cap_cj : ncap;
-    L.cap_pool = L.cap_pool > pcap ? L.cap_pool : pcap;
+    if (ncap > L.cap_cj) L.cap_cj = fl[1] + fl[1] / 2 + 32;
+    if (pcap > L.cap_pool) L.cap_pool = fl[2] + fl[2] / 2 + 8;
     if (nsci > 0) {
         L.tsci.ensure((size_t)NBX_NSHIFT * nsci);
         L.tcj.ensure((size_t)L.cap_cj * nsci);

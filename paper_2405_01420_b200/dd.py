@@ -674,6 +674,8 @@ def bench(args, METRIC, UNIT, FLOPS_PER_PAIR, DESC, ClockSampler, time_cpu_port,
     dist.barrier()
     torch.cuda.synchronize()
     l0 = dd.engine.launch_count()
+    a0 = dd.engine.nbx.lib().nbx_alloc_count()
+    seg0 = torch.cuda.memory_stats(dev).get("segment.all.allocated", 0)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     e0.record(st)
@@ -697,6 +699,8 @@ def bench(args, METRIC, UNIT, FLOPS_PER_PAIR, DESC, ClockSampler, time_cpu_port,
     dist.barrier()
     dd.check_peer()
     launches = dd.engine.launch_count() - l0
+    allocs = dd.engine.nbx.lib().nbx_alloc_count() - a0
+    segs = torch.cuda.memory_stats(dev).get("segment.all.allocated", 0) - seg0
     step_ms = [a.elapsed_time(b) for a, b in evs]
     era_ms, kind_ms, kind_n = compose_era(step_ms, kinds, s.nstlist, s.prune_every)
     t = torch.tensor([era_ms, e0.elapsed_time(e1) / K], dtype=torch.float64, device=dev)
@@ -774,6 +778,7 @@ def bench(args, METRIC, UNIT, FLOPS_PER_PAIR, DESC, ClockSampler, time_cpu_port,
                          "frac": value / 1e12 * fl / world / peak, "traffic": load_traffic(args.config, world),
                          "note": "per GPU, whole NB step (not kernel-only) at N>1"},
             "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
+            "device_allocs_in_timed_region_rank0": {"libnbx": int(allocs), "torch_segments": int(segs)},
             "step_ms_rank0": {"era": era_ms, "by_kind": kind_ms, "kind_counts": kind_n,
                               "window_mean_max_over_ranks": window_max},
             "dd_phases_ms_rank0": phases,

@@ -66,7 +66,7 @@ EXPORTS = ["nbx_last_error", "nbx_version", "nbx_derive_consts", "nbx_ewald_tabl
            "nbx_set_topology", "nbx_set_box", "nbx_grid_build", "nbx_search", "nbx_put_x",
            "nbx_prune", "nbx_force", "nbx_get_f", "nbx_step_graph", "nbx_energies", "nbx_clear_energies",
            "nbx_grid_info_get", "nbx_grid_export", "nbx_list_sizes_get", "nbx_list_export",
-           "nbx_count_pairs", "nbx_fma_peak", "nbx_launch_count", "nbx_halo_pack_x", "nbx_halo_unpack_add_f",
+           "nbx_count_pairs", "nbx_fma_peak", "nbx_launch_count", "nbx_alloc_count", "nbx_halo_pack_x", "nbx_halo_unpack_add_f",
            "nbx_peer_init", "nbx_peer_open", "nbx_peer_set_halo", "nbx_peer_put_x", "nbx_peer_halo_x",
            "nbx_peer_force_nonlocal", "nbx_peer_get_f", "nbx_peer_status",
            "nbx_pme_create", "nbx_pme_destroy", "nbx_pme_set_box", "nbx_pme_compute", "nbx_pme_energy",
@@ -110,6 +110,8 @@ def lib():
         L.nbx_fma_peak.argtypes = [vp, C.POINTER(C.c_double), vp]
         L.nbx_launch_count.argtypes = [vp]
         L.nbx_launch_count.restype = C.c_int64
+        L.nbx_alloc_count.argtypes = []
+        L.nbx_alloc_count.restype = C.c_int64
         L.nbx_halo_pack_x.argtypes = [vp, vp, i32, vp, vp, vp]
         L.nbx_halo_unpack_add_f.argtypes = [vp, vp, i32, vp, vp]
         L.nbx_peer_init.argtypes = [vp, i32, i32, i32, vp]
@@ -369,6 +371,11 @@ class Nonbonded:
 
     def launch_count(self):
         return lib().nbx_launch_count(self.ctx.h)
+
+    @staticmethod
+    def alloc_count():
+        """Device allocations made by libnbx so far (process-wide; none in steady state)."""
+        return lib().nbx_alloc_count()
 
     def close(self):
         self.ctx.close()

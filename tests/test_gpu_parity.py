@@ -422,3 +422,34 @@ def test_combination_rule_table_check(gpu):
         nbx.Nonbonded(s, device=0)
     s.lj_modifier = "comb-lb"
     nbx.Nonbonded(s, device=0)  # LB-mixed: accepted
+
+
+@pytest.mark.parametrize("name", SMALL + ["stmv"])
+def test_entry_order_longest_first(gpu, name, monkeypatch):
+    """Row f2 (post-prune list sort by length; the reference's HIP prune_sort
+    task, /root/reference/pkg/src/mdgpusim/pipeline.py:236-240): with the longest-first
+    processing order the force kernel visits the same inner list in another order, so forces,
+    energies and virial still match the oracle (the list itself is unchanged, bit-exact), after
+    a search and after a moved-atom prune + graph step."""
+    import torch
+    monkeypatch.setenv("NBX_ENTRY_ORDER", "1")  # read by nbx_create
+    s = get_system(name, 200000 if name == "stmv" else None)
+    nb, on, xd = run_pair(s)
+    assert_lists_equal(nb.pairlist(1), on.list.export(1), f"{name} sorted-order inner")
+    f, (e, vir) = nb.forces(xd, energy=True, virial=True)
+    torch.cuda.synchronize()
+    fo, eo, viro, _ = on.forces()
+    assert_forces(f.cpu().numpy(), fo)
+    assert_energies(e, eo)
+    assert_virial(vir, viro)
+    rng = np.random.default_rng(5)
+    x1 = (s.x + rng.uniform(-0.02, 0.02, size=s.x.shape)).astype(np.float32)
+    x1d = to_dev(x1)
+    fg = torch.empty_like(x1d)
+    nb.graph_step(x1d, fg, prune=True)  # X op + prune (+ sort) + force + F op as one graph
+    torch.cuda.synchronize()
+    on.put_x(x1)
+    on.prune()
+    assert_lists_equal(nb.pairlist(1), on.list.export(1), f"{name} sorted-order pruned")
+    fo1, _, _, _ = on.forces()
+    assert_forces(fg.cpu().numpy(), fo1)

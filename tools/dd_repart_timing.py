@@ -27,11 +27,15 @@ def main():
     d.repartition(xg)
     d.step(None, step=1)
     runs = []
-    for _ in range(6):
+    g = torch.Generator(device=dev)
+    g.manual_seed(3)
+    for it in range(6):
+        # moved coordinates every other repartition (as between two searches of an MD run)
+        xr = xg if it % 2 == 0 else xg + 0.02 * torch.randn(xg.shape, device=dev, generator=g)
         d.timing = {}
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        d.repartition(xg)
+        d.repartition(xr)
         torch.cuda.synchronize()
         t1 = time.perf_counter()
         d.step(None, step=1, prune=False)
@@ -41,7 +45,7 @@ def main():
     for r in range(world):
         dist.barrier()
         if rank == r:
-            for tr, ts, tim in runs[-2:]:
+            for tr, ts, tim in runs:
                 print(f"rank {rank}: repartition {tr:.2f} ms, first step after {ts:.2f} ms: "
                       + ", ".join(f"{k} {1e3 * v:.2f}" for k, v in tim.items()), flush=True)
     dist.destroy_process_group()

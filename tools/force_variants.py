@@ -12,6 +12,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "scratch", "variants")
 VARIANTS = {
     "base": [],
+    "pairs": ["-DNBX_TILE_PAIRS=1"],
+    "pairs_u1": ["-DNBX_TILE_PAIRS=1", "-DNBX_EUNROLL=1"],
+    "u1": ["-DNBX_EUNROLL=1"],
+    "minb4": ["-DNBX_FORCE_MINB=4"],
+    "pairs_minb4": ["-DNBX_TILE_PAIRS=1", "-DNBX_FORCE_MINB=4"],
 }
 
 
