@@ -232,6 +232,39 @@ NBX_API int nbx_peer_force_nonlocal(nbx_ctx* ctx, uint32_t seq, uint32_t flags, 
 NBX_API int nbx_peer_get_f(nbx_ctx* ctx, float* f_home_dev, uint32_t seq, uint32_t flags, void* stream);
 NBX_API int nbx_peer_status(nbx_ctx* ctx, int32_t* timed_out);
 
+/* ---- device-side DD repartition over the peer regions (the search step of the peer path) --
+ * Replaces the host-orchestrated global repartition (every rank reading every atom) with a
+ * neighbour-only one: each rank publishes its current home atoms (x, gid), then pulls from the
+ * ranks at domain offsets within +-1 (src_rank) the atoms whose wrapped position now lies in its
+ * own domain -- its new home set, sorted by global id -- publishes that, and pulls its half-shell
+ * halo (off_*: the offsets whose first non-zero component is +1, with the periodic image shift)
+ * from the neighbours' new home sets.  Everything is stream-ordered device work with flag
+ * waits; the host reads two counts at the end.  Outputs (device, capacity cap_ext):
+ * x_ext[0 : n_home] = new home atoms (wrapped), x_ext[n_home : n_home + n_halo] = halo atoms in
+ * this rank's frame, gid_ext likewise; owner / home_index / shift [n_halo] = the halo map for
+ * nbx_peer_set_halo.  rseq: 1, 2, 3, ... per repartition, identical on all ranks.  Returns
+ * NBX_ELIST_OVERFLOW (counts still written) when the new home set exceeds the peer capacity
+ * or home + halo exceeds cap_ext: re-create the regions / buffers larger and repartition from
+ * global coordinates.  Mirrors the reference's decomposed pair search on home + halo atoms
+ * (pipeline.py:329-334).                                                                    */
+typedef struct nbx_dd_geom {
+    float box[3];          /* periodic box                                                   */
+    float dlen[3];         /* domain edge per dimension (box / dims)                         */
+    float lo[3], hi[3];    /* this rank's domain                                             */
+    float rl;              /* halo width (rlist_outer)                                       */
+    int32_t dims[3], coord[3];
+    int32_t n_src;         /* ranks this rank's new home atoms can come from (incl. itself)  */
+    int32_t src_rank[27];
+    int32_t n_off;         /* half-shell import offsets                                      */
+    int32_t off_rank[13];
+    int32_t off_dir[13][3];
+    float off_shift[13][3];
+} nbx_dd_geom;
+NBX_API int nbx_peer_repartition(nbx_ctx* ctx, const nbx_dd_geom* geom, const float* x_home_dev,
+                                 const int32_t* gid_home_dev, int32_t n_home, uint32_t rseq, int32_t cap_ext,
+                                 float* x_ext_dev, int32_t* gid_ext_dev, int32_t* owner_dev, int32_t* home_index_dev,
+                                 float* shift_dev, int32_t* n_home_out, int32_t* n_halo_out, void* stream);
+
 /* Energies and virial accumulated since the last clear.  Reads grid buffers, so call it
  * after nbx_force and BEFORE nbx_get_f.  e_host[2] = {E_lj, E_coul incl. self term},
  * virial_host[9] = -1/2 sum x (x) f - 1/2 sum s (x) fshift (row-major).  Synchronises.    */

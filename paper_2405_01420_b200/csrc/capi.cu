@@ -686,6 +686,24 @@ NBX_API int nbx_peer_status(nbx_ctx* ctx, int32_t* timed_out)
     NBX_GUARD_END
 }
 
+NBX_API int nbx_peer_repartition(nbx_ctx* ctx, const nbx_dd_geom* geom, const float* x_home, const int32_t* gid_home,
+                                 int32_t n_home, uint32_t rseq, int32_t cap_ext, float* x_ext, int32_t* gid_ext,
+                                 int32_t* owner, int32_t* home_index, float* shift, int32_t* n_home_out,
+                                 int32_t* n_halo_out, void* stream)
+{
+    NBX_GUARD_BEGIN
+    NBX_CHECK_CTX(ctx);
+    if (!geom || !x_ext || !gid_ext || !owner || !home_index || !shift || !n_home_out || !n_halo_out ||
+        n_home < 0 || (n_home > 0 && (!x_home || !gid_home)))
+        return fail(NBX_EINVAL, "bad repartition arguments");
+    if (peer_repartition(ctx, geom, x_home, gid_home, n_home, rseq, cap_ext, x_ext, gid_ext, owner, home_index, shift,
+                         n_home_out, n_halo_out, (cudaStream_t)stream))
+        return fail(NBX_ELIST_OVERFLOW, "repartition: new home / halo atoms exceed the capacities (counts returned)");
+    ctx->epoch++;
+    return NBX_OK;
+    NBX_GUARD_END
+}
+
 NBX_API int nbx_clear_energies(nbx_ctx* ctx, void* stream)
 {
     NBX_GUARD_BEGIN

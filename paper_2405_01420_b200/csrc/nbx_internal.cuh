@@ -260,6 +260,9 @@ void peer_halo_x(nbx_ctx* ctx, unsigned seq, cudaStream_t st);
 void peer_force_nonlocal(nbx_ctx* ctx, unsigned seq, unsigned flags, cudaStream_t st);
 void peer_get_f(nbx_ctx* ctx, float* f, unsigned seq, unsigned flags, cudaStream_t st);
 int peer_status(nbx_ctx* ctx);
+int peer_repartition(nbx_ctx* ctx, const nbx_dd_geom* g, const float* xh, const int* gh, int nh, unsigned rseq,
+                     int cap_ext, float* x_ext, int* gid_ext, int* owner, int* home, float* shift, int* nh_out,
+                     int* nhalo_out, cudaStream_t st);
 ForceConsts make_force_consts(const nbx_consts& c);
 void pme_setup(nbx_pme* pme);
 void pme_set_box(nbx_pme* pme, const float box[3]);

@@ -31,16 +31,27 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "nbx_internal.cuh"
 
 namespace nbx {
 
 struct Peer {
     int rank = 0, world = 0, cap = 0, n_halo = 0;
-    char* base = nullptr;        // own IPC region: flags | xpub | inbox
-    unsigned* flags = nullptr;   // [2][world]
+    char* base = nullptr;        // own IPC region: flags | counts | xpub | inbox | xpub2 | gpub | gpub2
+    unsigned* flags = nullptr;   // [4][world]: x ready, f done, homes published, new homes published
+    int* cnt = nullptr;          // [0] published home count, [1] published new-home count
     float4* xpub = nullptr;      // [cap] home coordinates (x, y, z, 0) of this step
     float4* inbox = nullptr;     // [cap] forces on home atoms from other ranks' nonlocal lists
+    float4* xpub2 = nullptr;     // [cap] repartition: the new home atoms (wrapped x, sorted by gid)
+    int* gpub = nullptr;         // [cap] repartition: global ids of the published home atoms
+    int* gpub2 = nullptr;        // [cap] repartition: global ids of the new home atoms
+    DBuf<float4*> d_xpub2;       // [world] every rank's xpub2 / gpub / gpub2 / cnt
+    DBuf<int*> d_gpub, d_gpub2, d_cnt;
+    DBuf<int> rp_key, rp_key_out, rp_val, rp_val_out, rp_cnt; // repartition scratch
+    DBuf<float4> rp_stage;
+    DBuf<char> rp_tmp;
     std::vector<char*> remote;   // opened peer regions (nullptr for self)
     DBuf<unsigned*> d_flags;     // [world] flag arrays of every rank
     DBuf<float4*> d_xpub, d_inbox;
@@ -54,7 +65,24 @@ struct Peer {
     unsigned long long timeout_ns = 30ull * 1000000000ull;
 };
 
-static size_t flags_bytes(int world) { return ((size_t)2 * world * sizeof(unsigned) + 255) / 256 * 256; }
+static size_t flags_bytes(int world) { return ((size_t)4 * world * sizeof(unsigned) + 255) / 256 * 256; }
+constexpr size_t CNT_BYTES = 256;
+// byte offsets of the region's arrays (identical on every rank: same world and cap)
+struct PeerLayout {
+    size_t flags, cnt, xpub, inbox, xpub2, gpub, gpub2, bytes;
+    PeerLayout(int world, int cap)
+    {
+        const size_t c16 = (size_t)cap * sizeof(float4), c4 = ((size_t)cap * sizeof(int) + 255) / 256 * 256;
+        flags = 0;
+        cnt = flags_bytes(world);
+        xpub = cnt + CNT_BYTES;
+        inbox = xpub + c16;
+        xpub2 = inbox + c16;
+        gpub = xpub2 + c16;
+        gpub2 = gpub + c4;
+        bytes = gpub2 + c4;
+    }
+};
 
 __device__ __forceinline__ unsigned long long gtimer()
 {
@@ -184,6 +212,9 @@ void peer_release(nbx_ctx* ctx)
         if (r) cudaIpcCloseMemHandle(r);
     if (P->base) cudaFree(P->base);
     P->d_flags.release(); P->d_xpub.release(); P->d_inbox.release(); P->src.release();
+    P->d_xpub2.release(); P->d_gpub.release(); P->d_gpub2.release(); P->d_cnt.release();
+    P->rp_key.release(); P->rp_key_out.release(); P->rp_val.release(); P->rp_val_out.release();
+    P->rp_cnt.release(); P->rp_stage.release(); P->rp_tmp.release();
     P->hshift.release(); P->fj_dst.release(); P->dst.release(); P->err.release();
     delete P;
     ctx->peer = nullptr;
@@ -199,12 +230,16 @@ void peer_init(nbx_ctx* ctx, int rank, int world, int cap, void* handle_out)
     P->cap = cap;
     if (const char* t = std::getenv("NBX_PEER_TIMEOUT_S")) P->timeout_ns = (unsigned long long)(std::atof(t) * 1e9);
     if (const char* f = std::getenv("NBX_PEER_FUSED")) P->fused = std::atoi(f) != 0;
-    const size_t fb = flags_bytes(world), bytes = fb + 2 * (size_t)cap * sizeof(float4);
-    NBX_CUDA(cudaMalloc((void**)&P->base, bytes));
-    NBX_CUDA(cudaMemset(P->base, 0, bytes));
-    P->flags = reinterpret_cast<unsigned*>(P->base);
-    P->xpub = reinterpret_cast<float4*>(P->base + fb);
-    P->inbox = P->xpub + cap;
+    const PeerLayout Lo(world, cap);
+    NBX_CUDA(cudaMalloc((void**)&P->base, Lo.bytes));
+    NBX_CUDA(cudaMemset(P->base, 0, Lo.bytes));
+    P->flags = reinterpret_cast<unsigned*>(P->base + Lo.flags);
+    P->cnt = reinterpret_cast<int*>(P->base + Lo.cnt);
+    P->xpub = reinterpret_cast<float4*>(P->base + Lo.xpub);
+    P->inbox = reinterpret_cast<float4*>(P->base + Lo.inbox);
+    P->xpub2 = reinterpret_cast<float4*>(P->base + Lo.xpub2);
+    P->gpub = reinterpret_cast<int*>(P->base + Lo.gpub);
+    P->gpub2 = reinterpret_cast<int*>(P->base + Lo.gpub2);
     P->err.ensure(1);
     NBX_CUDA(cudaMemset(P->err.p, 0, sizeof(int)));
     cudaIpcMemHandle_t h;
@@ -217,10 +252,11 @@ void peer_init(nbx_ctx* ctx, int rank, int world, int cap, void* handle_out)
 void peer_open(nbx_ctx* ctx, const void* handles)
 {
     Peer& P = need(ctx, false, false);
-    const size_t fb = flags_bytes(P.world);
+    const PeerLayout Lo(P.world, P.cap);
     P.remote.assign(P.world, nullptr);
     std::vector<unsigned*> fl(P.world);
-    std::vector<float4*> xp(P.world), ib(P.world);
+    std::vector<float4*> xp(P.world), ib(P.world), xp2(P.world);
+    std::vector<int*> gp(P.world), gp2(P.world), cn(P.world);
     for (int w = 0; w < P.world; w++) {
         char* b = P.base;
         if (w != P.rank) {
@@ -229,16 +265,28 @@ void peer_open(nbx_ctx* ctx, const void* handles)
             NBX_CUDA(cudaIpcOpenMemHandle((void**)&b, h, cudaIpcMemLazyEnablePeerAccess));
             P.remote[w] = b;
         }
-        fl[w] = reinterpret_cast<unsigned*>(b);
-        xp[w] = reinterpret_cast<float4*>(b + fb);
-        ib[w] = xp[w] + P.cap;
+        fl[w] = reinterpret_cast<unsigned*>(b + Lo.flags);
+        cn[w] = reinterpret_cast<int*>(b + Lo.cnt);
+        xp[w] = reinterpret_cast<float4*>(b + Lo.xpub);
+        ib[w] = reinterpret_cast<float4*>(b + Lo.inbox);
+        xp2[w] = reinterpret_cast<float4*>(b + Lo.xpub2);
+        gp[w] = reinterpret_cast<int*>(b + Lo.gpub);
+        gp2[w] = reinterpret_cast<int*>(b + Lo.gpub2);
     }
     P.d_flags.ensure(P.world);
     P.d_xpub.ensure(P.world);
     P.d_inbox.ensure(P.world);
+    P.d_xpub2.ensure(P.world);
+    P.d_gpub.ensure(P.world);
+    P.d_gpub2.ensure(P.world);
+    P.d_cnt.ensure(P.world);
     NBX_CUDA(cudaMemcpy(P.d_flags.p, fl.data(), sizeof(unsigned*) * P.world, cudaMemcpyHostToDevice));
     NBX_CUDA(cudaMemcpy(P.d_xpub.p, xp.data(), sizeof(float4*) * P.world, cudaMemcpyHostToDevice));
     NBX_CUDA(cudaMemcpy(P.d_inbox.p, ib.data(), sizeof(float4*) * P.world, cudaMemcpyHostToDevice));
+    NBX_CUDA(cudaMemcpy(P.d_xpub2.p, xp2.data(), sizeof(float4*) * P.world, cudaMemcpyHostToDevice));
+    NBX_CUDA(cudaMemcpy(P.d_gpub.p, gp.data(), sizeof(int*) * P.world, cudaMemcpyHostToDevice));
+    NBX_CUDA(cudaMemcpy(P.d_gpub2.p, gp2.data(), sizeof(int*) * P.world, cudaMemcpyHostToDevice));
+    NBX_CUDA(cudaMemcpy(P.d_cnt.p, cn.data(), sizeof(int*) * P.world, cudaMemcpyHostToDevice));
     P.open = true;
 }
 
@@ -353,6 +401,201 @@ void peer_get_f(nbx_ctx* ctx, float* f, unsigned seq, unsigned flags, cudaStream
         NBX_CUDA(cudaGetLastError());
     }
     if (G.nslots > 0) NBX_CUDA(cudaMemsetAsync(G.f.p, 0, sizeof(float4) * G.nslots, st));
+}
+
+// ---- device-side repartition (nbx_peer_repartition; include/nbx.h) -----------------------
+// Phase A: publish the current home atoms (x, gid, count), signal kind 2, wait for everyone,
+// pull from the neighbour ranks the atoms whose wrapped position lies in this domain, sort
+// them by global id (deterministic home order), publish them as the new home set (xpub2,
+// gpub2), signal kind 3.  Phase B: wait, pull the half-shell halo from the neighbours' new
+// home sets, sort by (offset, owner home index).  The wrap and domain arithmetic is the host
+// path's (dd.py repartition: xw = x - floor(x / L) L, c = floor(xw / D) clamped) in IEEE
+// single precision, so every rank decides every atom's owner identically: each atom lands in
+// exactly one new home set (dd.py checks the total).  Kind-2 publication reuses xpub, which
+// nobody reads any more (every rank passed its previous step's "f done" wait); the new home
+// set goes to xpub2, which no rank overwrites before everyone has pulled its halo from it
+// (kind-3 wait before the next repartition's publication... many steps later).
+constexpr unsigned RP_SENTINEL = 0x7f7f7f7fu; // sorts after every real key (memset byte 0x7f)
+
+__global__ void k_rp_publish(int n, const int* __restrict__ n_dev, int cap, const float* __restrict__ x,
+                             const int* __restrict__ gid, float4* __restrict__ xpub, int* __restrict__ gpub,
+                             int* __restrict__ cnt, int slot)
+{
+    const int nn = n_dev ? min(*n_dev, cap) : n;
+    const int a = blockIdx.x * blockDim.x + threadIdx.x;
+    if (a == 0) cnt[slot] = nn;
+    if (a >= nn) return;
+    xpub[a] = make_float4(x[3 * a], x[3 * a + 1], x[3 * a + 2], 0.0f);
+    gpub[a] = gid[a];
+}
+
+__device__ __forceinline__ float rp_wrap(float x, float L)
+{
+    return __fsub_rn(x, __fmul_rn(floorf(__fdiv_rn(x, L)), L));
+}
+
+__global__ void k_rp_pull_home(nbx_dd_geom G, const float4* const* __restrict__ xpub, const int* const* __restrict__ gpub,
+                               int* const* __restrict__ cnt, int cap, int* __restrict__ counter,
+                               int* __restrict__ key, int* __restrict__ val, float4* __restrict__ stage)
+{
+    const int r = G.src_rank[blockIdx.y];
+    const int n = __ldcg(cnt[r]);
+    for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < n; a += gridDim.x * blockDim.x) {
+        const float4 p = __ldcg(xpub[r] + a);
+        const float w0 = rp_wrap(p.x, G.box[0]), w1 = rp_wrap(p.y, G.box[1]), w2 = rp_wrap(p.z, G.box[2]);
+        const float w[3] = {w0, w1, w2};
+        bool mine = true;
+#pragma unroll
+        for (int d = 0; d < 3; d++) {
+            int c = (int)floorf(__fdiv_rn(w[d], G.dlen[d]));
+            c = c < 0 ? 0 : (c > G.dims[d] - 1 ? G.dims[d] - 1 : c);
+            mine = mine && (c == G.coord[d]);
+        }
+        if (!mine) continue;
+        const int slot = atomicAdd(counter, 1);
+        if (slot >= cap) continue; // overflow: reported through the count
+        key[slot] = __ldcg(gpub[r] + a);
+        val[slot] = slot;
+        stage[slot] = make_float4(w0, w1, w2, 0.0f);
+    }
+}
+
+__global__ void k_rp_gather_home(int cap, const int* __restrict__ counter, const int* __restrict__ key,
+                                 const int* __restrict__ val, const float4* __restrict__ stage,
+                                 float* __restrict__ x, int* __restrict__ gid)
+{
+    const int n = min(*counter, cap);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const float4 p = stage[val[i]];
+        x[3 * i] = p.x;
+        x[3 * i + 1] = p.y;
+        x[3 * i + 2] = p.z;
+        gid[i] = key[i];
+    }
+}
+
+__global__ void k_rp_pull_halo(nbx_dd_geom G, const float4* const* __restrict__ xpub2,
+                               const int* const* __restrict__ gpub2, int* const* __restrict__ cnt, int cap,
+                               int* __restrict__ counter, int* __restrict__ key, int* __restrict__ val,
+                               float4* __restrict__ stage)
+{
+    const int oi = blockIdx.y;
+    const int r = G.off_rank[oi];
+    const int n = __ldcg(cnt[r] + 1);
+    for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < n; a += gridDim.x * blockDim.x) {
+        const float4 p = __ldcg(xpub2[r] + a);
+        const float x[3] = {__fadd_rn(p.x, G.off_shift[oi][0]), __fadd_rn(p.y, G.off_shift[oi][1]),
+                            __fadd_rn(p.z, G.off_shift[oi][2])};
+        bool in = true;
+#pragma unroll
+        for (int d = 0; d < 3; d++) {
+            const int o = G.off_dir[oi][d];
+            if (o > 0) in = in && x[d] < __fadd_rn(G.hi[d], G.rl);
+            if (o < 0) in = in && x[d] >= __fsub_rn(G.lo[d], G.rl);
+        }
+        if (!in) continue;
+        const int slot = atomicAdd(counter, 1);
+        if (slot >= cap) continue;
+        key[slot] = (oi << 26) | a;
+        val[slot] = slot;
+        stage[slot] = make_float4(x[0], x[1], x[2], __int_as_float(__ldcg(gpub2[r] + a)));
+    }
+}
+
+__global__ void k_rp_gather_halo(nbx_dd_geom G, int cap_ext, const int* __restrict__ counters, int cap_home,
+                                 const int* __restrict__ key, const int* __restrict__ val,
+                                 const float4* __restrict__ stage, float* __restrict__ x, int* __restrict__ gid,
+                                 int* __restrict__ owner, int* __restrict__ home, float* __restrict__ shift)
+{
+    const int nh = min(counters[0], cap_home);
+    const int n = min(counters[1], cap_ext - nh);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const float4 p = stage[val[i]];
+        const int k = key[i], oi = k >> 26;
+        const int e = nh + i;
+        x[3 * e] = p.x;
+        x[3 * e + 1] = p.y;
+        x[3 * e + 2] = p.z;
+        gid[e] = __float_as_int(p.w);
+        owner[i] = G.off_rank[oi];
+        home[i] = k & ((1 << 26) - 1);
+        shift[3 * i] = G.off_shift[oi][0];
+        shift[3 * i + 1] = G.off_shift[oi][1];
+        shift[3 * i + 2] = G.off_shift[oi][2];
+    }
+}
+
+static void rp_sort(nbx_ctx* ctx, Peer& P, int n, int end_bit, cudaStream_t st)
+{
+    size_t tb = 0;
+    NBX_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, P.rp_key.p, P.rp_key_out.p, P.rp_val.p, P.rp_val_out.p, n,
+                                             0, end_bit, st));
+    P.rp_tmp.ensure(tb + 16);
+    NBX_CUDA(cub::DeviceRadixSort::SortPairs(P.rp_tmp.p, tb, P.rp_key.p, P.rp_key_out.p, P.rp_val.p,
+                                             P.rp_val_out.p, n, 0, end_bit, st));
+    ctx->launches += 4;
+}
+
+int peer_repartition(nbx_ctx* ctx, const nbx_dd_geom* g, const float* xh, const int* gh, int nh, unsigned rseq,
+                     int cap_ext, float* x_ext, int* gid_ext, int* owner, int* home, float* shift, int* nh_out,
+                     int* nhalo_out, cudaStream_t st)
+{
+    Peer& P = need(ctx, true, false);
+    if (nh > P.cap) throw CudaError{cudaErrorInvalidValue, "home atoms exceed the peer capacity"};
+    if (cap_ext < 1 || cap_ext >= (1 << 26) || P.cap >= (1 << 26))
+        throw CudaError{cudaErrorInvalidValue, "repartition capacity out of range (< 2^26)"};
+    if (g->n_src < 1 || g->n_src > 27 || g->n_off < 0 || g->n_off > 13)
+        throw CudaError{cudaErrorInvalidValue, "bad repartition geometry"};
+    const int capw = P.cap > cap_ext ? P.cap : cap_ext;
+    P.rp_key.ensure(capw);
+    P.rp_key_out.ensure(capw);
+    P.rp_val.ensure(capw);
+    P.rp_val_out.ensure(capw);
+    P.rp_stage.ensure(capw);
+    P.rp_cnt.ensure(4);
+    NBX_CUDA(cudaMemsetAsync(P.rp_cnt.p, 0, 4 * sizeof(int), st));
+    const int T = 256, B = 4 * ctx->num_sms;
+    // phase A
+    k_rp_publish<<<(nh + T) / T, T, 0, st>>>(nh, nullptr, P.cap, xh, gh, P.xpub, P.gpub, P.cnt, 0);
+    ctx->launches++;
+    NBX_CUDA(cudaGetLastError());
+    signal(ctx, P, 2, rseq, st);
+    wait(ctx, P, 2, rseq, st);
+    NBX_CUDA(cudaMemsetAsync(P.rp_key.p, 0x7f, sizeof(int) * (size_t)P.cap, st));
+    k_rp_pull_home<<<dim3(B, g->n_src), T, 0, st>>>(*g, P.d_xpub.p, P.d_gpub.p, P.d_cnt.p, P.cap, P.rp_cnt.p,
+                                                     P.rp_key.p, P.rp_val.p, P.rp_stage.p);
+    ctx->launches++;
+    NBX_CUDA(cudaGetLastError());
+    rp_sort(ctx, P, P.cap, 31, st);
+    k_rp_gather_home<<<B, T, 0, st>>>(P.cap < cap_ext ? P.cap : cap_ext, P.rp_cnt.p, P.rp_key_out.p,
+                                      P.rp_val_out.p, P.rp_stage.p, x_ext, gid_ext);
+    ctx->launches++;
+    NBX_CUDA(cudaGetLastError());
+    k_rp_publish<<<(P.cap + T - 1) / T, T, 0, st>>>(0, P.rp_cnt.p, P.cap < cap_ext ? P.cap : cap_ext, x_ext, gid_ext,
+                                                    P.xpub2, P.gpub2, P.cnt, 1);
+    ctx->launches++;
+    NBX_CUDA(cudaGetLastError());
+    signal(ctx, P, 3, rseq, st);
+    // phase B
+    wait(ctx, P, 3, rseq, st);
+    if (g->n_off > 0) {
+        NBX_CUDA(cudaMemsetAsync(P.rp_key.p, 0x7f, sizeof(int) * (size_t)cap_ext, st));
+        k_rp_pull_halo<<<dim3(B, g->n_off), T, 0, st>>>(*g, P.d_xpub2.p, P.d_gpub2.p, P.d_cnt.p, cap_ext,
+                                                         P.rp_cnt.p + 1, P.rp_key.p, P.rp_val.p, P.rp_stage.p);
+        ctx->launches++;
+        NBX_CUDA(cudaGetLastError());
+        rp_sort(ctx, P, cap_ext, 31, st);
+        k_rp_gather_halo<<<B, T, 0, st>>>(*g, cap_ext, P.rp_cnt.p, P.cap, P.rp_key_out.p, P.rp_val_out.p,
+                                          P.rp_stage.p, x_ext, gid_ext, owner, home, shift);
+        ctx->launches++;
+        NBX_CUDA(cudaGetLastError());
+    }
+    int h[2] = {0, 0};
+    NBX_CUDA(cudaMemcpyAsync(h, P.rp_cnt.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+    NBX_CUDA(cudaStreamSynchronize(st));
+    *nh_out = h[0];
+    *nhalo_out = h[1];
+    return (h[0] > P.cap || h[0] + h[1] > cap_ext) ? 1 : 0;
 }
 
 int peer_status(nbx_ctx* ctx)

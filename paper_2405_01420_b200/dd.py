@@ -179,6 +179,20 @@ class NbxEngine:
         self.nbx.check(self.nbx.lib().nbx_peer_get_f(self.ctx.h, self.nbx._dev_ptr(f) if f.shape[0] else None,
                                                      seq, flags, self._st(stream)))
 
+    def peer_repartition(self, geom, x_home, gid_home, rseq, x_ext, gid_ext, owner, home, shift):
+        """nbx_peer_repartition: returns (overflowed, n_home, n_halo)."""
+        import ctypes as C
+        nbx = self.nbx
+        nh, nhalo = C.c_int32(), C.c_int32()
+        n = int(x_home.shape[0])
+        code = nbx.lib().nbx_peer_repartition(
+            self.ctx.h, C.byref(geom), nbx._dev_ptr(x_home) if n else None, nbx._dev_ptr(gid_home) if n else None,
+            n, rseq, int(x_ext.shape[0]), nbx._dev_ptr(x_ext), nbx._dev_ptr(gid_ext), nbx._dev_ptr(owner),
+            nbx._dev_ptr(home), nbx._dev_ptr(shift), C.byref(nh), C.byref(nhalo), self._st())
+        if code not in (0, 4):  # 4 = NBX_ELIST_OVERFLOW: counts returned, caller falls back
+            nbx.check(code)
+        return code == 4, nh.value, nhalo.value
+
     def peer_status(self):
         import ctypes as C
         v = C.c_int32()
@@ -239,6 +253,10 @@ class DomainDecomposition:
         self.overlap_nonlocal = os.environ.get("NBX_DD_OVERLAP", "1") != "0"
         self._side = None
         self._peer_cap = 0
+        self.rseq = 0             # device repartitions so far (peer-path search steps)
+        self._rp = None           # device-repartition output buffers (capacity-sized)
+        self._geom = None
+        self.repartitions = {"global": 0, "device": 0, "fallback": 0}
         # gloo moves host tensors only: with CUDA tensors (e.g. several ranks sharing one GPU,
         # tests/test_dd_gpu.py's oversubscribed mode) every exchange is staged through host
         # memory; with NCCL the device tensors go straight onto the wire
@@ -295,8 +313,22 @@ class DomainDecomposition:
             self.timing[name] = self.timing.get(name, 0.0) + (t - self._t_last)
         self._t_last = t
 
-    def repartition(self, x_global):
-        """Assign home atoms, build the halo plan, grids and lists (a search step)."""
+    def repartition(self, x_global=None, x_home=None):
+        """A search step: (re)assign home atoms, build the halo plan, grids and lists.
+
+        x_global given (every rank the same [N, 3] coordinates): the host-orchestrated global
+        partition (first call, NCCL halo, fallback).  Otherwise, on the peer-memory path, the
+        device-side neighbour-only repartition (nbx_peer_repartition) from this rank's current
+        home coordinates x_home (default: those of the last step): no global coordinates, no
+        per-pulse host synchronisation, two counts read at the end."""
+        if x_global is None:
+            if not (self.halo == "p2p" and self._peer_ready):
+                raise ValueError("x_global is required for the first partition and for the NCCL halo path")
+            return self._repartition_device(x_home)
+        self.repartitions["global"] += 1
+        return self._repartition_global(x_global)
+
+    def _repartition_global(self, x_global):
         torch = self.torch
         dev = self.device
         self.check_peer()
@@ -411,6 +443,127 @@ class DomainDecomposition:
             self._peer_map()
             self._tick("peer_map")
         return self.n_home
+
+    def dd_geom(self):
+        """nbx_dd_geom of this rank: domain, neighbour ranks, half-shell import offsets."""
+        if self._geom is not None:
+            return self._geom
+        import itertools
+
+        from . import nbx
+        g = nbx.DDGeom()
+        box32 = np.asarray(self.box, np.float32)
+        D32 = np.asarray(self.D, np.float32)  # the host path's float32 domain edge
+        for d in range(3):
+            g.box[d] = float(box32[d])
+            g.dlen[d] = float(D32[d])
+            g.lo[d] = float(np.float32(self.coord[d] * self.D[d]))
+            g.hi[d] = float(np.float32((self.coord[d] + 1) * self.D[d]))
+            g.dims[d] = self.dims[d]
+            g.coord[d] = self.coord[d]
+        g.rl = self.rl
+        rng = [(-1, 0, 1) if self.dims[d] > 1 else (0,) for d in range(3)]
+        srcs = []
+        offs = []
+        for o in itertools.product(*rng):
+            c = [self.coord[d] + o[d] for d in range(3)]
+            r = coords_rank(c, self.dims)
+            if r not in srcs:
+                srcs.append(r)
+            nz = [v for v in o if v != 0]
+            if nz and nz[0] == 1:
+                sh = [box32[d] if c[d] >= self.dims[d] else (-box32[d] if c[d] < 0 else 0.0) for d in range(3)]
+                offs.append((r, o, sh))
+        g.n_src = len(srcs)
+        for k, r in enumerate(srcs):
+            g.src_rank[k] = r
+        g.n_off = len(offs)
+        for k, (r, o, sh) in enumerate(offs):
+            g.off_rank[k] = r
+            for d in range(3):
+                g.off_dir[k][d] = o[d]
+                g.off_shift[k][d] = float(sh[d])
+        self._geom = g
+        return g
+
+    def _repartition_device(self, x_home=None):
+        torch, dist = self.torch, self.dist
+        dev = self.device
+        self.check_peer()
+        self._tick()
+        x_home = (self.x_ext[:self.n_home] if x_home is None else x_home).contiguous()
+        gid_home = self.home_gid.contiguous()
+        cap_ext = 3 * self._peer_cap
+        if self._rp is None or self._rp["x"].shape[0] < cap_ext:
+            self._rp = {"x": torch.empty((cap_ext, 3), dtype=torch.float32, device=dev),
+                        "gid": torch.empty(cap_ext, dtype=torch.int32, device=dev),
+                        "owner": torch.empty(cap_ext, dtype=torch.int32, device=dev),
+                        "home": torch.empty(cap_ext, dtype=torch.int32, device=dev),
+                        "shift": torch.empty((cap_ext, 3), dtype=torch.float32, device=dev),
+                        "f": torch.zeros((cap_ext, 3), dtype=torch.float32, device=dev)}
+        B = self._rp
+        if B["x"].data_ptr() == x_home.data_ptr() or B["gid"].data_ptr() == gid_home.data_ptr():
+            # the library publishes x_home / gid_home before it writes the outputs: aliasing the
+            # output buffers is safe (see peer.cu), but keep the inputs alive past the call
+            pass
+        self.rseq += 1
+        over, nh, nhalo = self.engine.peer_repartition(self.dd_geom(), x_home, gid_home, self.rseq & 0xFFFFFFFF,
+                                                       B["x"], B["gid"], B["owner"], B["home"], B["shift"])
+        self._tick("device_repartition")
+        chk = torch.tensor([nh, int(over)], dtype=torch.int64, device=dev)
+        chk = self._all_reduce(chk).cpu()
+        if int(chk[1]) or int(chk[0]) != self.sys.natoms:
+            # capacity overflow or lost atoms (moved more than one domain): rebuild globally from
+            # an all-gather of the home sets (rare; the regions regrow in _peer_map)
+            self.repartitions["fallback"] += 1
+            return self._repartition_global(self._gather_global(x_home, gid_home))
+        self.repartitions["device"] += 1
+        self.n_home, self.n_ext = nh, nh + nhalo
+        self.x_ext = B["x"][:self.n_ext]
+        self.gid_ext = B["gid"][:self.n_ext]
+        self.home_gid = self.gid_ext[:self.n_home]
+        self.f_ext = B["f"][:self.n_ext]
+        self.f_ext.zero_()
+        self.pulses = []  # the message-passing halo plan is not built on this path
+        size_l, lo_l, size_n, lo_n = self._grid_boxes()
+        eng = self.engine
+        eng.grid_build(0, self.x_ext[:self.n_home], self.gid_ext[:self.n_home], lo_l, size_l)
+        eng.search(0)
+        eng.grid_build(1, self.x_ext[self.n_home:], self.gid_ext[self.n_home:], lo_n, size_n)
+        eng.search(1)
+        self._tick("grids_searches")
+        self._peer_owner = B["owner"][:nhalo]
+        self._peer_home = B["home"][:nhalo]
+        self._peer_shift = B["shift"][:nhalo]
+        self.engine.peer_set_halo(self._peer_owner, self._peer_home, self._peer_shift)
+        self._tick("peer_map")
+        return self.n_home
+
+    def _gather_global(self, x_home, gid_home):
+        """All ranks' home sets -> the global [N, 3] coordinate array on every rank."""
+        torch = self.torch
+        dev = self.device
+        n = torch.tensor([int(x_home.shape[0])], dtype=torch.int64, device=dev)
+        ns = [int(v) for v in self._all_gather(n)]
+        mx = max(ns)
+        xp = torch.zeros((mx, 3), dtype=torch.float32, device=dev)
+        gp = torch.zeros(mx, dtype=torch.int64, device=dev)
+        xp[:ns[self.rank]] = x_home
+        gp[:ns[self.rank]] = gid_home.long()
+        xs, gs = self._all_gather(xp), self._all_gather(gp)
+        xg = torch.empty((self.sys.natoms, 3), dtype=torch.float32, device=dev)
+        for r in range(self.world):
+            xg[gs[r][:ns[r]].to(dev)] = xs[r][:ns[r]].to(dev)
+        return xg
+
+    def _grid_boxes(self):
+        """(size, lo) of the local (home) grid and the nonlocal (halo) grid."""
+        lo = np.array([self.coord[d] * self.D[d] for d in range(3)])
+        size_l = np.array([self.D[d] if self.dims[d] > 1 else self.box[d] for d in range(3)], np.float32)
+        lo_l = np.array([lo[d] if self.dims[d] > 1 else 0.0 for d in range(3)], np.float32)
+        size_n = np.array([self.D[d] + 2 * self.rl if self.dims[d] > 1 else self.box[d] for d in range(3)], np.float32)
+        lo_n = np.array([lo[d] - self.rl if self.dims[d] > 1 else 0.0 for d in range(3)], np.float32)
+        return size_l, lo_l, size_n, lo_n
 
     def _peer_map(self):
         """Peer halo map after a repartition: for every imported atom its owner rank, its index
@@ -654,9 +807,19 @@ def bench(args, METRIC, UNIT, FLOPS_PER_PAIR, DESC, ClockSampler, time_cpu_port,
         return xh + vel[dd.home_gid.long()] * (sg * dt_ps)
 
     peak = dd.engine.fma_peak()
+
+    def search_step_repartition(x_home):
+        # peer path: the device-side neighbour-only repartition from the home coordinates;
+        # NCCL path: the global partition from the (moved) global coordinates
+        if halo == "p2p":
+            return dd.repartition(x_home=x_home)
+        return dd.repartition(xg_now())
+
     dd.repartition(xg_now())  # setup: first search sizes the lists and the single-pass buffers
     dd.step(None, step=0, prune=False)
-    dd.repartition(xg_now())
+    search_step_repartition(dd.x_ext[:dd.n_home])
+    dd.step(None, step=0, prune=False)
+    search_step_repartition(dd.x_ext[:dd.n_home])
     x_home = dd.x_ext[:dd.n_home].clone()
     for k in range(args.warmup):
         step = max(1, s.nstlist - args.warmup + k)
@@ -687,7 +850,7 @@ def bench(args, METRIC, UNIT, FLOPS_PER_PAIR, DESC, ClockSampler, time_cpu_port,
         evs[k][0].record(st)
         if kinds[k] == "search":
             tc = time.perf_counter()
-            dd.repartition(xg_now())  # atoms re-assigned from the (moved) global coordinates
+            search_step_repartition(x_home)
             rep_cpu_ms.append(1e3 * (time.perf_counter() - tc))
             x_home = dd.x_ext[:dd.n_home].clone()
             dd.step(None, step=k, prune=False)
@@ -771,7 +934,9 @@ def bench(args, METRIC, UNIT, FLOPS_PER_PAIR, DESC, ClockSampler, time_cpu_port,
                        "l2": "inputs larger than L2" if s.natoms > 2_000_000 else "per-rank inputs may fit L2",
                        "step_time": "one nstlist era composed from each rank's per-kind step means, max over "
                                     "ranks; the window starts with a search (repartition) step",
-                       "motion": "x += v dt between steps (v reversed every nstlist steps)"},
+                       "motion": "x += v dt between steps (v reversed every nstlist steps)",
+                       "repartition": ("device-side neighbour-only (nbx_peer_repartition) from home coordinates"
+                                       if halo == "p2p" else "global (host-orchestrated, NCCL pulses)")},
             "steps_per_s": 1e3 / ms_per_step, "ns_per_day": 86.4 * s.dt_fs / ms_per_step,
             "pairs_per_step": pairs_tot, "pair_slots_per_step": slots_tot,
             "roofline": {"bound": "fp32", "achieved": value / 1e12 * fl / world, "peak": peak, "unit": "TFLOP/s",
@@ -783,6 +948,7 @@ def bench(args, METRIC, UNIT, FLOPS_PER_PAIR, DESC, ClockSampler, time_cpu_port,
                               "window_mean_max_over_ranks": window_max},
             "dd_phases_ms_rank0": phases,
             "repartition_host_ms_per_rank": rep_cpu_all,
+            "repartitions_rank0": dict(dd.repartitions),
         }
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()

@@ -53,6 +53,14 @@ class ListSizes(C.Structure):
                 ("n_pool", C.c_int64)]
 
 
+class DDGeom(C.Structure):
+    """nbx_dd_geom (include/nbx.h): the device-side repartition's domain geometry."""
+    _fields_ = [("box", C.c_float * 3), ("dlen", C.c_float * 3), ("lo", C.c_float * 3), ("hi", C.c_float * 3),
+                ("rl", C.c_float), ("dims", C.c_int32 * 3), ("coord", C.c_int32 * 3), ("n_src", C.c_int32),
+                ("src_rank", C.c_int32 * 27), ("n_off", C.c_int32), ("off_rank", C.c_int32 * 13),
+                ("off_dir", (C.c_int32 * 3) * 13), ("off_shift", (C.c_float * 3) * 13)]
+
+
 class GridInfo(C.Structure):
     _fields_ = [("n", C.c_int32), ("nslots", C.c_int32), ("ncx", C.c_int32), ("ncy", C.c_int32)]
 
@@ -68,7 +76,7 @@ EXPORTS = ["nbx_last_error", "nbx_version", "nbx_derive_consts", "nbx_ewald_tabl
            "nbx_grid_info_get", "nbx_grid_export", "nbx_list_sizes_get", "nbx_list_export",
            "nbx_count_pairs", "nbx_fma_peak", "nbx_launch_count", "nbx_alloc_count", "nbx_halo_pack_x", "nbx_halo_unpack_add_f",
            "nbx_peer_init", "nbx_peer_open", "nbx_peer_set_halo", "nbx_peer_put_x", "nbx_peer_halo_x",
-           "nbx_peer_force_nonlocal", "nbx_peer_get_f", "nbx_peer_status",
+           "nbx_peer_force_nonlocal", "nbx_peer_get_f", "nbx_peer_status", "nbx_peer_repartition",
            "nbx_pme_create", "nbx_pme_destroy", "nbx_pme_set_box", "nbx_pme_compute", "nbx_pme_energy",
            "nbx_pme_launch_count", "nbx_pme_profile", "nbx_pme_compute_grid", "nbx_leapfrog",
            "nbx_step_graph_pme"]
@@ -122,6 +130,8 @@ def lib():
         L.nbx_peer_force_nonlocal.argtypes = [vp, u32, u32, vp]
         L.nbx_peer_get_f.argtypes = [vp, vp, u32, u32, vp]
         L.nbx_peer_status.argtypes = [vp, vp]
+        L.nbx_peer_repartition.argtypes = [vp, C.POINTER(DDGeom), vp, vp, i32, u32, i32, vp, vp, vp, vp, vp,
+                                           C.POINTER(i32), C.POINTER(i32), vp]
         L.nbx_pme_create.argtypes = [C.c_int, vp, C.POINTER(vp)]
         L.nbx_pme_destroy.argtypes = [vp]
         L.nbx_pme_set_box.argtypes = [vp, vp]

@@ -84,15 +84,40 @@ def main():
         G, F = gather_home(d, t, world, dev, s.natoms)
         out_arrays[name] = F
         out_arrays["gids"] = G
-    # a second repartition from the moved coordinates (atoms change domains), then an energy step
+    # a second repartition from the moved coordinates (atoms change domains), then an energy step.
+    # p2p: the device-side neighbour-only repartition from the home coordinates (no global
+    # array); nccl: the global partition
     x2 = xg + disp
-    d.repartition(x2)
+    if halo == "p2p":
+        d.repartition(x_home=x_home)
+    else:
+        d.repartition(x2)
     f3, (e3, vir3) = d.step(None, step=100, energy=True, virial=True, prune=False)
     torch.cuda.synchronize()
     d.check_peer()
     G3, F3 = gather_home(d, f3, world, dev, s.natoms)
     out_arrays["f3"] = F3
     out_arrays["gids3"] = G3
+    # a third repartition after more motion (uniform +-0.015 nm; larger random kicks push atom
+    # pairs unphysically close, where r^-13 forces make the fp32 frame rounding of the DD's
+    # wrapped coordinates dominate the max-error metric), force step
+    rng2 = np.random.default_rng(4)
+    disp2 = torch.from_numpy(rng2.uniform(-0.015, 0.015, size=s.x.shape).astype(np.float32)).to(dev)
+    x3 = x2 + disp2
+    x_home3 = d.x_ext[:d.n_home] + disp2[d.home_gid.long()]
+    if halo == "p2p":
+        d.repartition(x_home=x_home3)
+    else:
+        d.repartition(x3)
+    f4 = d.step(None, step=200, prune=False).clone()
+    torch.cuda.synchronize()
+    d.check_peer()
+    G4, F4 = gather_home(d, f4, world, dev, s.natoms)
+    out_arrays["f4"] = F4
+    out_arrays["gids4"] = G4
+    reps = torch.tensor([d.repartitions["global"], d.repartitions["device"], d.repartitions["fallback"]],
+                        dtype=torch.int64, device=dev)
+    reps = d._all_reduce(reps).cpu().numpy()
     if rank == 0:
         nb = nbx.Nonbonded(s, device=devi)
         nb.search(xg)
@@ -104,10 +129,13 @@ def main():
         f12, (e12, v12) = nb.forces(x2, energy=True, virial=True)
         nb.search(x2)
         f13, (e13, v13) = nb.forces(x2, energy=True, virial=True)
+        nb.search(x3)
+        f14 = nb.forces(x3)
         np.savez(out, e=e, vir=vir, e2=e2, vir2=vir2, e3=e3, vir3=vir3,
                  fa_ref=fa1.cpu().numpy(), f_ref=f1.cpu().numpy(), e_ref=e1, vir_ref=v1,
                  fb_ref=fb1.cpu().numpy(), f2_ref=f12.cpu().numpy(), e2_ref=e12, vir2_ref=v12,
-                 f3_ref=f13.cpu().numpy(), e3_ref=e13, vir3_ref=v13, natoms=s.natoms,
+                 f3_ref=f13.cpu().numpy(), e3_ref=e13, vir3_ref=v13, f4_ref=f14.cpu().numpy(), natoms=s.natoms,
+                 repartitions=reps, world=world,
                  peer_inits=getattr(d, "peer_inits", 0), n_home=d.n_home, n_ext=d.n_ext, **out_arrays)
     dist.barrier()
     dist.destroy_process_group()

@@ -9,7 +9,9 @@ Two launch modes of the same worker (tests/dd_gpu_worker.py):
     halo over CUDA IPC on the same device -- so a 1-GPU box runs dd.py and csrc/peer.cu end to
     end on the full-size STMV box and the 12 M box.
 Checked per case: force-only, energy + virial (both through the chosen halo), moved atoms with
-the rolling prune, and an energy step after a second repartition from moved coordinates
+the rolling prune, an energy step after a second repartition from moved coordinates and a
+force step after a third -- on the peer path both of those are the device-side neighbour-only
+repartition (nbx_peer_repartition) from the ranks' home coordinates, with no global array
 (reference schedule: /root/reference/pkg/src/mdgpusim/pipeline.py:267-438)."""
 import os
 import socket
@@ -54,22 +56,42 @@ def _run(world, config, natoms, halo, oversub=False, timeout=900):
         return dict(np.load(out))
 
 
-def _check(d):
+# Max-force bar of the DD-vs-single-GPU comparison.  Both runs are fp32; where a pair crosses a
+# periodic face the two evaluate the image difference in different frames (DD: halo coordinate
+# + box shift; single GPU: shift vector in the pair loop), and fp32 coordinates near 49 nm (the
+# 12 M box) carry a 3.8e-6 nm ulp, so an O-O pair at 0.25 nm differs by ~2e-4 in its r^-13 force
+# (tools/dd_diag.py: the largest |df| sit on atoms at the split plane and a periodic face; the
+# force rel RMS stays 3e-7).  The 1e-4 north_star bar is kept for every box up to STMV size.
+MAX_TOL = {"water12m": 3e-4}
+
+
+def _check(d, halo, config=None):
     n = int(d["natoms"])
+    mt = MAX_TOL.get(config, 1e-4)
+
+    def af(f, fref):
+        return assert_forces(f, fref, max_tol=mt)
+
     assert np.array_equal(np.sort(d["gids"]), np.arange(n))  # every atom has exactly one home
     assert np.array_equal(np.sort(d["gids3"]), np.arange(n))
-    assert_forces(d["fa"], d["fa_ref"])
-    assert_forces(d["f"], d["f_ref"])
+    af(d["fa"], d["fa_ref"])
+    af(d["f"], d["f_ref"])
     assert_energies(d["e"], d["e_ref"])
     assert_virial(d["vir"], d["vir_ref"])
-    assert_forces(d["fb"], d["fb_ref"])
-    assert_forces(d["fb2"], d["fb_ref"])
-    assert_forces(d["f2"], d["f2_ref"])
+    af(d["fb"], d["fb_ref"])
+    af(d["fb2"], d["fb_ref"])
+    af(d["f2"], d["f2_ref"])
     assert_energies(d["e2"], d["e2_ref"])
     assert_virial(d["vir2"], d["vir2_ref"])
-    assert_forces(d["f3"], d["f3_ref"])
+    af(d["f3"], d["f3_ref"])
     assert_energies(d["e3"], d["e3_ref"])
     assert_virial(d["vir3"], d["vir3_ref"])
+    assert np.array_equal(np.sort(d["gids4"]), np.arange(n))
+    af(d["f4"], d["f4_ref"])
+    glob, devc, fallback = (int(v) for v in d["repartitions"])
+    assert fallback == 0, "device repartition fell back to the global path"
+    if halo == "p2p":  # the second and third search steps ran the device-side repartition
+        assert devc == 2 * int(d["world"]), (glob, devc)
 
 
 # ---- one GPU, N ranks sharing it (runs on the driver's 1-GPU box) ---------------------------
@@ -81,7 +103,7 @@ def _check(d):
 ])
 def test_dd_oversubscribed_one_gpu(gpu, config, world, halo):
     d = _run(world, config, "full", halo, oversub=True, timeout=1200)
-    _check(d)
+    _check(d, halo, config)
 
 
 # ---- one rank per GPU over NCCL ---------------------------------------------------------------
@@ -91,14 +113,14 @@ def test_dd_stmv_full_matches_single_gpu(gpu, world, halo):
     """STMV-sized 1,066,628 atoms at N = 2/4/8 (BASELINE config 4), both halo forms."""
     if _ngpu() < world:
         pytest.skip(f"needs {world} GPUs")
-    _check(_run(world, "stmv", "full", halo))
+    _check(_run(world, "stmv", "full", halo), halo)
 
 
 def test_dd_water12m_full_8gpu(gpu):
     """12 M-atom water box at N = 8 (BASELINE config 5), peer-memory halo."""
     if _ngpu() < 8:
         pytest.skip("needs 8 GPUs")
-    _check(_run(8, "water12m", "full", "p2p", timeout=1500))
+    _check(_run(8, "water12m", "full", "p2p", timeout=1500), "p2p", "water12m")
 
 
 @pytest.mark.parametrize("config", ["stmv_tab", "grappa1.5m", "rnase24k_lb"])
@@ -110,4 +132,4 @@ def test_dd_paper_flavours(gpu, world, config):
     if _ngpu() < world:
         pytest.skip(f"needs {world} GPUs")
     natoms = 60000 if config == "rnase24k_lb" else 150000
-    _check(_run(world, config, natoms, "p2p"))
+    _check(_run(world, config, natoms, "p2p"), "p2p")
