@@ -691,6 +691,110 @@ __global__ void __launch_bounds__(PRUNE_THREADS) k_prune_packed(PruneArgs A)
     }
 }
 
+// Fixed-lane prune (NBX_PRUNE_KERNEL=3): lane = i atom of the super-cluster (i-cluster lane / 4,
+// row lane % 4), its shifted coordinates in registers for the whole entry; the chunk's j atoms
+// staged structure-of-arrays (row t = 8 floats: the staging stores hit 32 consecutive words,
+// every read is a broadcast of one row).  Each cj entry is one warp-uniform pass: every lane
+// tests its i atom against the 8 j atoms with packed FP32x2 r^2 (two j atoms per FADD2 /
+// FMUL2 / FFMA2), one ballot, and the 32 hit bits fold into the entry's 8 i-cluster bits.
+// No item table, no shared atomics; inactive tiles (imask bit clear) are computed and
+// discarded, so it trades ~3/8 wasted lanes for the packed kernel's bookkeeping.  Same r^2
+// rounding (dx = xj - xi, the exact negation) and keep rule: bit-identical lists.
+__global__ void __launch_bounds__(PRUNE_THREADS) k_prune_fixed(PruneArgs A)
+{
+    constexpr int W = PRUNE_THREADS / 32;
+    __shared__ __align__(16) float s_j[W][3][32][8];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int e = A.part + A.nparts * w;
+    if (e >= A.n_sci) return;
+    const unsigned full = 0xffffffffu, lt = (1u << lane) - 1u;
+    const nbx_sci_entry se = A.sci[e];
+    const int kk = lane >> 2, ii = lane & 3;
+    f2x AX, AY, AZ;
+    {
+        const float3 v = shift_vec(se.shift, A.box);
+        const float4 t0 = A.xq_i[32 * se.sci + lane];
+        AX = bc(__fadd_rn(t0.x, v.x));
+        AY = bc(__fadd_rn(t0.y, v.y));
+        AZ = bc(__fadd_rn(t0.z, v.z));
+    }
+    int kept = 0;
+    for (int c0 = se.cj_start; c0 < se.cj_end; c0 += 32) {
+        const int cnt = min(32, se.cj_end - c0);
+        nbx_cj_entry my;
+        my.cj = 0;
+        my.meta = 0u;
+        if (lane < cnt) my = A.cj[c0 + lane];
+        __syncwarp();
+        for (int r = 0; r < 8 && 4 * r < cnt; r++) {
+            const int t = 4 * r + (lane >> 3);
+            const int cjt = __shfl_sync(full, my.cj, t);
+            if (t < cnt) {
+                const int j = lane & 7;
+                const float4 b = A.xq_j[8 * cjt + j];
+                s_j[wib][0][t][j] = b.x;
+                s_j[wib][1][t][j] = b.y;
+                s_j[wib][2][t][j] = b.z;
+            }
+        }
+        __syncwarp();
+        unsigned my_nm = 0u;
+        for (int t = 0; t < cnt; t++) {
+            const unsigned meta = __shfl_sync(full, my.meta, t);
+            const unsigned pidx = meta >> 8;
+            const float* xs = s_j[wib][0][t];
+            const float* ys = s_j[wib][1][t];
+            const float* zs = s_j[wib][2][t];
+            float R[8];
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const ulonglong2 X = *reinterpret_cast<const ulonglong2*>(xs + 4 * h);
+                const ulonglong2 Y = *reinterpret_cast<const ulonglong2*>(ys + 4 * h);
+                const ulonglong2 Z = *reinterpret_cast<const ulonglong2*>(zs + 4 * h);
+                const f2x DX0 = sub2(X.x, AX), DY0 = sub2(Y.x, AY), DZ0 = sub2(Z.x, AZ);
+                const f2x DX1 = sub2(X.y, AX), DY1 = sub2(Y.y, AY), DZ1 = sub2(Z.y, AZ);
+                const float2 R0 = upk(fma2(DZ0, DZ0, fma2(DY0, DY0, mul2(DX0, DX0))));
+                const float2 R1 = upk(fma2(DZ1, DZ1, fma2(DY1, DY1, mul2(DX1, DX1))));
+                R[4 * h] = R0.x;
+                R[4 * h + 1] = R0.y;
+                R[4 * h + 2] = R1.x;
+                R[4 * h + 3] = R1.y;
+            }
+            if (pidx) { // warp-uniform: the entry holds an excluded pair; masked pairs never keep a tile
+                const unsigned row = ((A.pool[pidx].m[kk][0] | A.pool[pidx].m[kk][1]) >> (8 * ii)) & 0xffu;
+                const float inf = __int_as_float(0x7f800000);
+#pragma unroll
+                for (int q = 0; q < 8; q++) R[q] = ((row >> q) & 1u) ? R[q] : inf;
+            }
+            const float r2min = fminf(fminf(fminf(R[0], R[1]), fminf(R[2], R[3])),
+                                      fminf(fminf(R[4], R[5]), fminf(R[6], R[7])));
+            const unsigned bits = __ballot_sync(full, r2min < A.rli2);
+            // bit 4k of f = OR of bits 4k..4k+3 (i-cluster k hit), gathered into bit k
+            unsigned f = bits | (bits >> 1);
+            f = (f | (f >> 2)) & 0x11111111u;
+            f = (f | (f >> 3)) & 0x03030303u;
+            f = (f | (f >> 6)) & 0x000f000fu;
+            f = (f | (f >> 12)) & 0xffu;
+            if (lane == t) my_nm = f & meta & 0xffu;
+        }
+        const unsigned keep = __ballot_sync(full, my_nm != 0u);
+        if (my_nm) {
+            nbx_cj_entry o;
+            o.cj = my.cj;
+            o.meta = my_nm | (my.meta & ~0xffu);
+            A.cj_in[se.cj_start + kept + __popc(keep & lt)] = o;
+        }
+        kept += __popc(keep);
+        __syncwarp();
+    }
+    if (lane == 0) {
+        nbx_sci_entry o = se;
+        o.cj_end = se.cj_start + kept;
+        A.sci_in[e] = o;
+    }
+}
+
 // count interacting in-cut-off pairs and pair slots of the inner list (bench denominator)
 __global__ void __launch_bounds__(256) k_count_pairs(PruneArgs A, float rc2, unsigned long long* out)
 {
@@ -814,6 +918,7 @@ void prune(nbx_ctx* ctx, int l, int part, int nparts, cudaStream_t st)
     const int blocks = (nw * 32 + PRUNE_THREADS - 1) / PRUNE_THREADS;
     if (ctx->prune_kernel == 0) k_prune<<<blocks, PRUNE_THREADS, 0, st>>>(A);
     else if (ctx->prune_kernel == 1) k_prune_lanes<<<blocks, PRUNE_THREADS, 0, st>>>(A);
+    else if (ctx->prune_kernel == 3) k_prune_fixed<<<blocks, PRUNE_THREADS, 0, st>>>(A);
     else k_prune_packed<<<blocks, PRUNE_THREADS, 0, st>>>(A); // default
     ctx->launches++;
     NBX_CUDA(cudaGetLastError());
