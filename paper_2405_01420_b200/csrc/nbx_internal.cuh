@@ -151,7 +151,8 @@ struct nbx_ctx {
     // first (sorted after every prune), -1 = auto (default): longest first for lists of
     // 1,024 <= n_sci < 32 x the resident force warps, where the tail matters and L2 locality
     // does not yet (measured: mem82k -7.5 %, STMV -1.8 % force kernel; 12 M +5 %, water 3k's
-    // ~10 us sort is not repaid).  Env NBX_ENTRY_ORDER overrides.
+    // ~10 us sort is not repaid), analytical Ewald / RF only (tabulated Ewald: +2.9 %).
+    // Env NBX_ENTRY_ORDER overrides.
     int entry_order = -1;
     // nbx_step_graph: natively captured X op (+ prune) + force + F op, one per (x, f, what);
     // `epoch` is bumped by every call that can move list/grid buffers or change constants,

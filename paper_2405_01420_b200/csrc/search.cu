@@ -884,6 +884,9 @@ __global__ void k_entry_len(const nbx_sci_entry* __restrict__ sci, int n, unsign
 static bool entry_order_on(const nbx_ctx* ctx, const List& L)
 {
     if (ctx->entry_order >= 0) return ctx->entry_order != 0;
+    // tabulated Ewald: the sorted order measured slower (STMV flavour +2.9 %, Grappa +0.3 % with
+    // the sort's cost on prune steps; profiles/r02_entry_order*.jsonl)
+    if (ctx->p.coulomb_type == NBX_COULOMB_EWALD_TAB) return false;
     const int64_t warps = (int64_t)ctx->num_sms * 3 * 8;
     return L.n_sci >= 1024 && L.n_sci < 32 * warps;
 }
