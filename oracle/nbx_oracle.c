@@ -153,9 +153,8 @@ static const float EW_GP[6] = {0.752252758f, -0.0231583007f, 0.0169008784f, 9.68
                                3.47007081e-05f, -3.8098932e-07f};
 static const float EW_GQ[6] = {1.0f, 0.569215298f, 0.149706319f, 0.0235451832f, 0.00233585062f,
                                0.000141900193f};
-static const float EW_HP[6] = {1.12837911f, 0.247148007f, 0.0558719411f, 0.0053259111f,
-                               0.000147049155f, -1.03906586e-06f};
-static const float EW_HQ[5] = {1.0f, 0.552361727f, 0.133642003f, 0.0178242605f, 0.00125038647f};
+static const float EW_HP[7] = {1.12837923f, 0.182699338f, 0.0532767773f, 0.00366060762f, 0.000346426154f, 3.80142114e-06f, -8.10354006e-09f};
+static const float EW_HQ[6] = {1.0f, 0.49524644f, 0.112297274f, 0.0149619607f, 0.00122577278f, 5.49911565e-05f};
 
 float ora_ewald_G(float z)
 {
@@ -166,9 +165,9 @@ float ora_ewald_G(float z)
 
 float ora_ewald_H(float z)
 {
-    float n = EW_HP[5], d = EW_HQ[4];
-    for (int k = 4; k >= 0; k--) n = fmaf(n, z, EW_HP[k]);
-    for (int k = 3; k >= 0; k--) d = fmaf(d, z, EW_HQ[k]);
+    float n = EW_HP[6], d = EW_HQ[5];
+    for (int k = 5; k >= 0; k--) n = fmaf(n, z, EW_HP[k]);
+    for (int k = 4; k >= 0; k--) d = fmaf(d, z, EW_HQ[k]);
     return n / d;
 }
 

@@ -119,7 +119,7 @@ struct ForceConsts {
     unsigned one;    // 1, opaque to the compiler: integer adds issued as IMAD (FMA pipe)
     float ewn[6], ewd[5]; // F-only Ewald: -beta^3 G as N(r2) / D(r2), D monic (pairmath.cuh)
     alignas(8) float ewnd[10]; // (ewn[k], ewd[k]) interleaved: one 64-bit constant per FFMA2
-    alignas(8) float ehnd[10]; // energy kernels' H(z) rational: (num, den) coefficient pairs
+    alignas(8) float ehnd[12]; // energy kernels' H(z) rational: (num, den) coefficient pairs
 };
 
 } // namespace nbx

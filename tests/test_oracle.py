@@ -32,7 +32,7 @@ def test_ewald_rational_accuracy():
     g = np.array([O.ewald_G(v) for v in z])
     h = np.array([O.ewald_H(v) for v in z])
     assert np.max(np.abs(g - G_exact(z)) / G_exact(z)) < 6e-7
-    assert np.max(np.abs(h - H_exact(z)) / H_exact(z)) < 6e-7
+    assert np.max(np.abs(h - H_exact(z)) / H_exact(z)) < 3.5e-7  # (6,5) fit, fp32 evaluation
 
 
 @pytest.mark.parametrize("name,n,coul_tol", [("water3k", None, 2e-6), ("rnase24k", 4000, 5e-5),

@@ -73,8 +73,8 @@ def eval32(p, q, z):
 
 if __name__ == "__main__":
     zt = np.linspace(0, ZMAX, 200001)
-    for name, f, (n, m) in (("G", G_exact, (5, 5)), ("H", H_exact, (5, 4))):
-        p, q = fit_rational(f, n, m)
+    for name, f, (n, m) in (("G", G_exact, (5, 5)), ("H", H_exact, (6, 5))):
+        p, q = fit_rational(f, n, m, iters=60)
         ref = f(zt)
         approx = eval32(p, q, zt).astype(np.float64)
         rel = np.abs(approx - ref) / np.abs(ref)
