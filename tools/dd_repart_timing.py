@@ -35,7 +35,10 @@ def main():
         d.timing = {}
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        d.repartition(xr)
+        if os.environ.get("NBX_REPART", "global") == "device" and d.halo == "p2p":
+            d.repartition(x_home=d.x_ext[:d.n_home])  # device-side neighbour-only repartition
+        else:
+            d.repartition(xr)
         torch.cuda.synchronize()
         t1 = time.perf_counter()
         d.step(None, step=1, prune=False)
