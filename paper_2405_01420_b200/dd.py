@@ -502,10 +502,8 @@ class DomainDecomposition:
                         "shift": torch.empty((cap_ext, 3), dtype=torch.float32, device=dev),
                         "f": torch.zeros((cap_ext, 3), dtype=torch.float32, device=dev)}
         B = self._rp
-        if B["x"].data_ptr() == x_home.data_ptr() or B["gid"].data_ptr() == gid_home.data_ptr():
-            # the library publishes x_home / gid_home before it writes the outputs: aliasing the
-            # output buffers is safe (see peer.cu), but keep the inputs alive past the call
-            pass
+        # x_home / gid_home may be views of B (the previous repartition's output): the library
+        # publishes them before it writes the outputs (peer.cu), so the aliasing is safe
         self.rseq += 1
         over, nh, nhalo = self.engine.peer_repartition(self.dd_geom(), x_home, gid_home, self.rseq & 0xFFFFFFFF,
                                                        B["x"], B["gid"], B["owner"], B["home"], B["shift"])
