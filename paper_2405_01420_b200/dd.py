@@ -493,6 +493,15 @@ class DomainDecomposition:
         self._tick()
         x_home = (self.x_ext[:self.n_home] if x_home is None else x_home).contiguous()
         gid_home = self.home_gid.contiguous()
+        B = self._rp
+        if B is not None:
+            # the inputs may be views of the output buffers (the previous repartition's
+            # result): the library publishes them before writing the outputs, but an overflow
+            # falls back to the global path, which needs the inputs intact -- copy them
+            if x_home.data_ptr() >= B["x"].data_ptr() and x_home.data_ptr() < B["x"].data_ptr() + B["x"].nbytes:
+                x_home = x_home.clone()
+            if gid_home.data_ptr() >= B["gid"].data_ptr() and gid_home.data_ptr() < B["gid"].data_ptr() + B["gid"].nbytes:
+                gid_home = gid_home.clone()
         cap_ext = 3 * self._peer_cap
         if self._rp is None or self._rp["x"].shape[0] < cap_ext:
             self._rp = {"x": torch.empty((cap_ext, 3), dtype=torch.float32, device=dev),
@@ -502,8 +511,6 @@ class DomainDecomposition:
                         "shift": torch.empty((cap_ext, 3), dtype=torch.float32, device=dev),
                         "f": torch.zeros((cap_ext, 3), dtype=torch.float32, device=dev)}
         B = self._rp
-        # x_home / gid_home may be views of B (the previous repartition's output): the library
-        # publishes them before it writes the outputs (peer.cu), so the aliasing is safe
         self.rseq += 1
         over, nh, nhalo = self.engine.peer_repartition(self.dd_geom(), x_home, gid_home, self.rseq & 0xFFFFFFFF,
                                                        B["x"], B["gid"], B["owner"], B["home"], B["shift"])
@@ -550,8 +557,13 @@ class DomainDecomposition:
         gp[:ns[self.rank]] = gid_home.long()
         xs, gs = self._all_gather(xp), self._all_gather(gp)
         xg = torch.empty((self.sys.natoms, 3), dtype=torch.float32, device=dev)
+        seen = torch.zeros(self.sys.natoms, dtype=torch.int32, device=dev)
         for r in range(self.world):
-            xg[gs[r][:ns[r]].to(dev)] = xs[r][:ns[r]].to(dev)
+            g = gs[r][:ns[r]].to(dev)
+            xg[g] = xs[r][:ns[r]].to(dev)
+            seen.index_add_(0, g, torch.ones_like(g, dtype=torch.int32))
+        if not bool((seen == 1).all()):
+            raise RuntimeError("DD fallback: the ranks' home sets do not partition the atoms")
         return xg
 
     def _grid_boxes(self):
@@ -577,7 +589,10 @@ class DomainDecomposition:
         nmax = torch.tensor([self.n_home], dtype=torch.int64, device=dev)
         nmax = int(self._all_reduce(nmax, op=dist.ReduceOp.MAX)[0])
         if not self._peer_ready or nmax > self._peer_cap:
-            cap = max(int(math.ceil(1.5 * self.sys.natoms / self.world)) + 4096, int(math.ceil(1.25 * nmax)))
+            # capacity: 1.5x the mean home count (env NBX_PEER_CAP_FACTOR; tests shrink it to force
+            # a regrow) and at least 1.25x the current largest home set
+            fac = float(os.environ.get("NBX_PEER_CAP_FACTOR", "1.5"))
+            cap = max(int(math.ceil(fac * self.sys.natoms / self.world)) + 4096, int(math.ceil(1.25 * nmax)))
             if self._peer_ready:
                 torch.cuda.synchronize(dev)  # nobody still reads / reduces into the old regions
                 dist.barrier(group=self.group)

@@ -106,6 +106,27 @@ def test_dd_oversubscribed_one_gpu(gpu, config, world, halo):
     _check(d, halo, config)
 
 
+def test_dd_peer_capacity_regrow_one_gpu(gpu):
+    """A device-side repartition whose new home set outgrows the peer regions: overflow ->
+    global fallback -> the regions are re-created larger on all ranks -> single-GPU forces,
+    energies and virial (tests/dd_regrow_worker.py)."""
+    with tempfile.TemporaryDirectory() as tmp:
+        out = os.path.join(tmp, "rg.npz")
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+               "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+               os.path.join(ROOT, "tests", "dd_regrow_worker.py"), out]
+        env = dict(os.environ, OMP_NUM_THREADS="2", NBX_PEER_CAP_FACTOR="1.0")
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
+        assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+        d = dict(np.load(out))
+    assert np.array_equal(np.sort(d["gids"]), np.arange(int(d["natoms"])))
+    assert int(d["fallback"]) == 1 and int(d["peer_inits"]) == 2
+    assert int(d["nmax"]) > int(d["cap0"]) and int(d["cap1"]) >= int(d["nmax"])
+    assert_forces(d["f"], d["f_ref"])
+    assert_energies(d["e"], d["e_ref"])
+    assert_virial(d["vir"], d["vir_ref"])
+
+
 # ---- one rank per GPU over NCCL ---------------------------------------------------------------
 @pytest.mark.parametrize("halo", ["nccl", "p2p"])
 @pytest.mark.parametrize("world", [2, 4, 8])
