@@ -230,7 +230,7 @@ NBX_API int nbx_peer_put_x(nbx_ctx* ctx, const float* x_home_dev, uint32_t seq, 
 NBX_API int nbx_peer_halo_x(nbx_ctx* ctx, uint32_t seq, void* stream);
 NBX_API int nbx_peer_force_nonlocal(nbx_ctx* ctx, uint32_t seq, uint32_t flags, void* stream);
 NBX_API int nbx_peer_get_f(nbx_ctx* ctx, float* f_home_dev, uint32_t seq, uint32_t flags, void* stream);
-NBX_API int nbx_peer_status(nbx_ctx* ctx, int32_t* timed_out);
+NBX_API int nbx_peer_status(nbx_ctx* ctx, int32_t* timed_out); /* 0 ok, 1 wait timed out, 2 invalid halo map */
 
 /* ---- device-side DD repartition over the peer regions (the search step of the peer path) --
  * Replaces the host-orchestrated global repartition (every rank reading every atom) with a

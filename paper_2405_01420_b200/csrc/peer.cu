@@ -172,15 +172,25 @@ __global__ void k_peer_push(int n, const int* __restrict__ islot, const float4* 
     const int a = blockIdx.x * blockDim.x + threadIdx.x;
     if (a >= n) return;
     const float4 v = fc[islot[a]];
-    red_add_v4(dst[a], make_float4(v.x, v.y, v.z, 0.f));
+    float4* d = dst[a];
+    if (d) red_add_v4(d, make_float4(v.x, v.y, v.z, 0.f)); // null: an invalid map entry (err 2)
 }
 
 __global__ void k_peer_src(int n, const int* __restrict__ owner, const int* __restrict__ home,
                            const float* __restrict__ shift, float4* const* xpub, float4* const* inbox,
-                           const float4** src, float4** dst, float4* hshift)
+                           const float4** src, float4** dst, float4* hshift, int world, int cap, int* err)
 {
     const int a = blockIdx.x * blockDim.x + threadIdx.x;
     if (a >= n) return;
+    if (owner[a] < 0 || owner[a] >= world || home[a] < 0 || home[a] >= cap) {
+        // a halo map pointing outside the peer regions: never dereference it (the step's
+        // gather / push would read or reduce into foreign memory); nbx_peer_status reports 2
+        atomicExch(err, 2);
+        src[a] = xpub[0];
+        dst[a] = nullptr;
+        hshift[a] = make_float4(0.f, 0.f, 0.f, 0.f);
+        return;
+    }
     src[a] = xpub[owner[a]] + home[a];
     dst[a] = inbox[owner[a]] + home[a];
     hshift[a] = make_float4(shift[3 * a], shift[3 * a + 1], shift[3 * a + 2], 0.f);
@@ -306,7 +316,7 @@ void peer_set_halo(nbx_ctx* ctx, int n, const int* owner, const int* home, const
     P.fj_dst.ensure(G1.nslots > 0 ? G1.nslots : 1);
     if (n > 0) {
         k_peer_src<<<(n + 255) / 256, 256, 0, st>>>(n, owner, home, shift, P.d_xpub.p, P.d_inbox.p, P.src.p,
-                                                     P.dst.p, P.hshift.p);
+                                                     P.dst.p, P.hshift.p, P.world, P.cap, P.err.p);
         ctx->launches++;
         NBX_CUDA(cudaGetLastError());
     }

@@ -614,9 +614,14 @@ class DomainDecomposition:
         dist.barrier(group=self.group)
 
     def check_peer(self):
-        """Raise if a peer-memory wait timed out (a rank stopped taking steps)."""
-        if self.halo == "p2p" and self._peer_ready and self.engine.peer_status():
-            raise RuntimeError("peer-memory halo: a wait for another rank timed out")
+        """Raise if a peer-memory wait timed out (a rank stopped taking steps) or the halo map
+        pointed outside the peer regions."""
+        if self.halo == "p2p" and self._peer_ready:
+            st = self.engine.peer_status()
+            if st == 1:
+                raise RuntimeError("peer-memory halo: a wait for another rank timed out")
+            if st:
+                raise RuntimeError("peer-memory halo: invalid halo map (owner / home index out of range)")
 
     # ---------------------------------------------------------------------- per step
     def halo_x(self):
