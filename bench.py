@@ -447,6 +447,9 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
+    # all the host threads: torchrun (N > 1) exports OMP_NUM_THREADS=1 to every rank; the oracle's
+    # OpenMP runtime reads the variable when it is first loaded, which happens below
+    os.environ["OMP_NUM_THREADS"] = str(len(os.sched_getaffinity(0)))
     t0 = time.perf_counter()
     r = time_cpu_port(args.config, None, steps=args.steps, warmup=args.warmup)
     wall = time.perf_counter() - t0

@@ -1037,14 +1037,18 @@ void search(nbx_ctx* ctx, int l, cudaStream_t st)
         ctx->launches++;
         NBX_CUDA(cudaGetLastError());
     }
-    // capacities for the next single pass: 25 % headroom over this search's maxima, and when
-    // that exceeds the current capacity, grow to 50 % headroom, so that the private buffers
-    // (nsci x cap, reallocated outside the next search) are not regrown every few searches as
-    // atoms move: a regrow is a multi-GB cudaFree + cudaMalloc (tens of ms, and it contends
-    // with NVML polls for the driver lock)
-    const int ncap = fl[1] + fl[1] / 4 + 32, pcap = fl[2] + fl[2] / 4 + 8;
-    if (ncap > L.cap_cj) L.cap_cj = fl[1] + fl[1] / 2 + 32;
-    if (pcap > L.cap_pool) L.cap_pool = fl[2] + fl[2] / 2 + 8;
+    // capacities for the next single pass: 50 % headroom over this search's maxima.  The private
+    // buffers (nsci x cap) are reallocated outside the next search; a regrow is a multi-GB
+    // cudaFree + cudaMalloc (tens of ms, and it contends with NVML polls for the driver lock).
+    // Regrown only after a search that did not fit (fl[0]: it fell back to count + fill, which
+    // needs no private buffers), or on the first: a regrow inside an MD run is a rare event tied
+    // to a search that was slow anyway (round 2: regrowing whenever 25 % headroom was lost cost
+    // a multi-GB reallocation every few hundred steps on some DD ranks)
+    if (L.cap_cj == 0 || fl[0]) {
+        const int ncap = fl[1] + fl[1] / 2 + 32, pcap = fl[2] + fl[2] / 2 + 8;
+        if (ncap > L.cap_cj) L.cap_cj = ncap;
+        if (pcap > L.cap_pool) L.cap_pool = pcap;
+    }
     if (nsci > 0) {
         L.tsci.ensure((size_t)NBX_NSHIFT * nsci);
         L.tcj.ensure((size_t)L.cap_cj * nsci);

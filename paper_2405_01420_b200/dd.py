@@ -882,6 +882,10 @@ def bench(args, METRIC, UNIT, FLOPS_PER_PAIR, DESC, ClockSampler, time_cpu_port,
     launches = dd.engine.launch_count() - l0
     allocs = dd.engine.nbx.lib().nbx_alloc_count() - a0
     segs = torch.cuda.memory_stats(dev).get("segment.all.allocated", 0) - seg0
+    al = torch.tensor([allocs, segs], dtype=torch.int64, device=dev)
+    al_all = [torch.zeros_like(al) for _ in range(world)]
+    dist.all_gather(al_all, al)
+    allocs_per_rank = [[int(v) for v in a.tolist()] for a in al_all]
     step_ms = [a.elapsed_time(b) for a, b in evs]
     era_ms, kind_ms, kind_n = compose_era(step_ms, kinds, s.nstlist, s.prune_every)
     t = torch.tensor([era_ms, e0.elapsed_time(e1) / K], dtype=torch.float64, device=dev)
@@ -961,7 +965,7 @@ def bench(args, METRIC, UNIT, FLOPS_PER_PAIR, DESC, ClockSampler, time_cpu_port,
                          "frac": value / 1e12 * fl / world / peak, "traffic": load_traffic(args.config, world),
                          "note": "per GPU, whole NB step (not kernel-only) at N>1"},
             "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
-            "device_allocs_in_timed_region_rank0": {"libnbx": int(allocs), "torch_segments": int(segs)},
+            "device_allocs_in_timed_region_per_rank": allocs_per_rank,  # [libnbx, torch segments]
             "step_ms_rank0": {"era": era_ms, "by_kind": kind_ms, "kind_counts": kind_n,
                               "window_mean_max_over_ranks": window_max},
             "dd_phases_ms_rank0": phases,
