@@ -12,11 +12,12 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "scratch", "variants")
 VARIANTS = {
     "base": [],
-    "pairs": ["-DNBX_TILE_PAIRS=1"],
-    "pairs_u1": ["-DNBX_TILE_PAIRS=1", "-DNBX_EUNROLL=1"],
-    "u1": ["-DNBX_EUNROLL=1"],
-    "minb4": ["-DNBX_FORCE_MINB=4"],
-    "pairs_minb4": ["-DNBX_TILE_PAIRS=1", "-DNBX_FORCE_MINB=4"],
+    "jred1": ["-DNBX_JRED16=1"],
+    "jred0": ["-DNBX_JRED16=0"],
+    "packf": ["-DNBX_TILE_PACKED_F=1"],
+    "leanlj": ["-DNBX_LEAN_LJ=1"],
+    "leancut": ["-DNBX_LEAN_CUT=1"],
+    "nolean": ["-DNBX_LEAN=0"],
 }
 
 
