@@ -12,12 +12,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "scratch", "variants")
 VARIANTS = {
     "base": [],
-    "jred1": ["-DNBX_JRED16=1"],
-    "jred0": ["-DNBX_JRED16=0"],
-    "packf": ["-DNBX_TILE_PACKED_F=1"],
-    "leanlj": ["-DNBX_LEAN_LJ=1"],
-    "leancut": ["-DNBX_LEAN_CUT=1"],
-    "nolean": ["-DNBX_LEAN=0"],
+    "large5": ["-DNBX_FORCE_MINB_LARGE=5"],
+    "large4u2": ["-DNBX_EUNROLL=2"],
+    "t128": ["-DNBX_FORCE_THREADS=128", "-DNBX_FORCE_MINB=6", "-DNBX_FORCE_MINB_LARGE=8"],
 }
 
 
