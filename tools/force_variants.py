@@ -12,9 +12,6 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "scratch", "variants")
 VARIANTS = {
     "base": [],
-    "large5": ["-DNBX_FORCE_MINB_LARGE=5"],
-    "large4u2": ["-DNBX_EUNROLL=2"],
-    "t128": ["-DNBX_FORCE_THREADS=128", "-DNBX_FORCE_MINB=6", "-DNBX_FORCE_MINB_LARGE=8"],
 }
 
 
@@ -40,7 +37,8 @@ def run_one(name, cfg, reps=20):
     sys.path.insert(0, ROOT)
     import torch
     from paper_2405_01420_b200 import nbx, systems
-    s = systems.make(cfg)
+    name, _, n = cfg.partition(":")
+    s = systems.make(name, int(n) if n else None)
     nb = nbx.Nonbonded(s)
     x = torch.from_numpy(s.x).cuda()
     f = torch.empty_like(x)
