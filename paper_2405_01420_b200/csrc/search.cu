@@ -557,9 +557,18 @@ __global__ void __launch_bounds__(PRUNE_THREADS) k_prune_lanes(PruneArgs A)
 // consecutive t (3 is coprime to 8), so a pass over <= 8 consecutive entries is conflict-free.
 // (Round 1's array-of-rows layout x[8] y[8] z[8] at stride 28 put rows t, t + 8 on the same
 // quads and its staging stores 2-way conflicted: 171 M conflicts per 12 M-atom prune.)
-constexpr int PRUNE_JS = 12;
+#ifndef NBX_PRUNE_JS
+// 8: rows unpadded (3 KB per warp).  The stride-12 layout above is bank-conflict-free for 8
+// consecutive rows but its 4.6 KB per warp costs occupancy: 12 M 3.90 -> 3.82 ms, STMV 0.607 ->
+// 0.594 ms with 8 (profiles/r02_prune_variants.jsonl)
+#define NBX_PRUNE_JS 8
+#endif
+#ifndef NBX_PRUNE_MINB
+#define NBX_PRUNE_MINB 1
+#endif
+constexpr int PRUNE_JS = NBX_PRUNE_JS;
 
-__global__ void __launch_bounds__(PRUNE_THREADS) k_prune_packed(PruneArgs A)
+__global__ void __launch_bounds__(PRUNE_THREADS, NBX_PRUNE_MINB) k_prune_packed(PruneArgs A)
 {
     constexpr int W = PRUNE_THREADS / 32;
     __shared__ __align__(16) float s_xj[W][3][32][PRUNE_JS];

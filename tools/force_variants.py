@@ -12,6 +12,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "scratch", "variants")
 VARIANTS = {
     "base": [],
+    "pjs8": ["-DNBX_PRUNE_JS=8"],
+    "pjs8m6": ["-DNBX_PRUNE_JS=8", "-DNBX_PRUNE_MINB=6"],
+    "pm6": ["-DNBX_PRUNE_MINB=6"],
 }
 
 
@@ -37,8 +40,8 @@ def run_one(name, cfg, reps=20):
     sys.path.insert(0, ROOT)
     import torch
     from paper_2405_01420_b200 import nbx, systems
-    name, _, n = cfg.partition(":")
-    s = systems.make(name, int(n) if n else None)
+    cname, _, n = cfg.partition(":")
+    s = systems.make(cname, int(n) if n else None)
     nb = nbx.Nonbonded(s)
     x = torch.from_numpy(s.x).cuda()
     f = torch.empty_like(x)
@@ -61,7 +64,13 @@ def run_one(name, cfg, reps=20):
     import numpy as np
     fn = f.cpu().numpy().astype(np.float64)
     np.save(os.path.join(OUT, f"f_{tag}_{cfg}.npy"), fn)
-    out = {"variant": tag, "config": cfg, "force_ms": ms, "slot_tflops": sl * 57 / ms / 1e9,
+    e0.record(st)
+    for _ in range(reps):
+        nb.prune()
+    e1.record(st)
+    torch.cuda.synchronize()
+    prune_ms = e0.elapsed_time(e1) / reps
+    out = {"variant": tag, "config": cfg, "force_ms": ms, "prune_ms": prune_ms, "slot_tflops": sl * 57 / ms / 1e9,
            "pairs_per_s": p / ms * 1e3}
     ref = os.path.join(OUT, f"f_base_{cfg}.npy")
     if os.path.exists(ref) and tag != "base":
