@@ -551,12 +551,13 @@ __global__ void __launch_bounds__(PRUNE_THREADS) k_prune_lanes(PruneArgs A)
 // pass runs two j atoms per FADD2 / FMUL2 / FFMA2 (the kernel is issue-bound with the FP32
 // pipe half idle).  dx = xj - xi is the exact negation of xi - xj, so every r^2 has the
 // scalar kernels' rounding and the keep rule is unchanged: bit-identical lists.
-// j atoms of a chunk, structure of arrays per coordinate: row t (entry t) = 8 floats at a
-// stride of 12 floats.  A pass reads one 16-byte quarter-row (h = 0, 1) of up to 8 distinct
-// rows per LDS.128: quarter (t, h) sits in bank quad (3 t + h) mod 8, distinct for 8
-// consecutive t (3 is coprime to 8), so a pass over <= 8 consecutive entries is conflict-free.
-// (Round 1's array-of-rows layout x[8] y[8] z[8] at stride 28 put rows t, t + 8 on the same
-// quads and its staging stores 2-way conflicted: 171 M conflicts per 12 M-atom prune.)
+// j atoms of a chunk, structure of arrays per coordinate: row t (entry t) = 8 floats at a stride
+// of NBX_PRUNE_JS floats.  A pass reads one 16-byte quarter-row (h = 0, 1) of up to 8 distinct
+// rows per LDS.128.  With a 12-float stride quarter (t, h) sits in bank quad (3 t + h) mod 8,
+// distinct for 8 consecutive t (conflict-free passes, and the staging stores no longer
+// conflict); unpadded (8 floats) rows t and t + 4 share a quad.  (Round 1's array-of-rows layout
+// x[8] y[8] z[8] at stride 28 put rows t, t + 8 on the same quads and its staging stores 2-way
+// conflicted: 171 M conflicts per 12 M-atom prune.)
 #ifndef NBX_PRUNE_JS
 // 8: rows unpadded (3 KB per warp).  The stride-12 layout above is bank-conflict-free for 8
 // consecutive rows but its 4.6 KB per warp costs occupancy: 12 M 3.90 -> 3.82 ms, STMV 0.607 ->
