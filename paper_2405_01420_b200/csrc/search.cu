@@ -144,7 +144,10 @@ __device__ __forceinline__ uint2 tile_eval(const SearchArgs& A, const WarpEx& X,
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(SEARCH_THREADS) k_search(SearchArgs A)
+#ifndef NBX_SEARCH_MINB
+#define NBX_SEARCH_MINB 1
+#endif
+__global__ void __launch_bounds__(SEARCH_THREADS, NBX_SEARCH_MINB) k_search(SearchArgs A)
 {
     __shared__ WarpEx s_ex[SEARCH_THREADS / 32];
     const int lane = threadIdx.x & 31;

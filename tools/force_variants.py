@@ -12,9 +12,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "scratch", "variants")
 VARIANTS = {
     "base": [],
-    "pjs8": ["-DNBX_PRUNE_JS=8"],
-    "pjs8m6": ["-DNBX_PRUNE_JS=8", "-DNBX_PRUNE_MINB=6"],
-    "pm6": ["-DNBX_PRUNE_MINB=6"],
+    "s10": ["-DNBX_SEARCH_MINB=10"],
+    "s12": ["-DNBX_SEARCH_MINB=12"],
+    "vf3": ["-DNBX_FORCE_MINB_ENERGY=3"],
 }
 
 
@@ -70,7 +70,19 @@ def run_one(name, cfg, reps=20):
     e1.record(st)
     torch.cuda.synchronize()
     prune_ms = e0.elapsed_time(e1) / reps
-    out = {"variant": tag, "config": cfg, "force_ms": ms, "prune_ms": prune_ms, "slot_tflops": sl * 57 / ms / 1e9,
+    e0.record(st)
+    for _ in range(3):
+        nb.search(x)
+    e1.record(st)
+    torch.cuda.synchronize()
+    search_ms = e0.elapsed_time(e1) / 3
+    e0.record(st)
+    for _ in range(3):
+        nb.compute(energy=True, virial=True)
+    e1.record(st)
+    torch.cuda.synchronize()
+    vf_ms = e0.elapsed_time(e1) / 3
+    out = {"variant": tag, "config": cfg, "force_ms": ms, "prune_ms": prune_ms, "search_ms": search_ms, "vf_ms": vf_ms, "slot_tflops": sl * 57 / ms / 1e9,
            "pairs_per_s": p / ms * 1e3}
     ref = os.path.join(OUT, f"f_base_{cfg}.npy")
     if os.path.exists(ref) and tag != "base":
