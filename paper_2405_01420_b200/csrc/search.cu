@@ -145,7 +145,10 @@ __device__ __forceinline__ uint2 tile_eval(const SearchArgs& A, const WarpEx& X,
 
 template <int MODE>
 #ifndef NBX_SEARCH_MINB
-#define NBX_SEARCH_MINB 1
+// 12 CTAs/SM (<= 42 registers, 48 warps): grid + search + prune of a search step 12 M 19.6 ->
+// 16.1 ms, STMV 2.58 -> 2.30 ms (RNase 24k +7 %, its search is launch-bound); 1 (64 registers)
+// was round 1's (profiles/r02_search_variants.jsonl)
+#define NBX_SEARCH_MINB 12
 #endif
 __global__ void __launch_bounds__(SEARCH_THREADS, NBX_SEARCH_MINB) k_search(SearchArgs A)
 {
