@@ -278,10 +278,11 @@ def run_single(args):
     dt_ps = s.dt_fs * 1e-3
     vel = torch.from_numpy(motion_velocities(s.natoms, s.nstlist, dt_ps)).cuda()
     zero_im = torch.zeros(s.natoms, dtype=torch.float32, device="cuda")  # inv_mass 0: v is kept
+    zero_f = torch.zeros_like(x)  # the update's force input (0 * f would still carry a NaN)
 
     def move(xx, step):
         # x += sign(step) v dt (HBM-bound, between the step events)
-        pme.leapfrog(xx, vel, f, zero_im, motion_sign(step, s.nstlist) * dt_ps)
+        pme.leapfrog(xx, vel, zero_f, zero_im, motion_sign(step, s.nstlist) * dt_ps)
 
     # small boxes are launch-bound: replay non-search steps as CUDA graphs
     graphs = s.natoms < 500_000
