@@ -27,6 +27,12 @@
 namespace nbx {
 
 constexpr int SEARCH_THREADS = 128;
+#ifndef NBX_SEARCH_V2
+// 1: phase B takes the i-cluster and survivor boxes from shared memory (staged once per sci /
+// per candidate chunk) and evaluates explicit tile masks cooperatively -- one tile per warp
+// pass, one atom pair per lane -- instead of 32 pairs serially in the owning lane
+#define NBX_SEARCH_V2 1
+#endif
 constexpr int EXMAX = 24; // partner j-clusters remembered per i-cluster (overflow -> always check)
 
 struct SearchArgs {
@@ -70,6 +76,10 @@ struct WarpEx {
     int cj[8][EXMAX];
     int n[8];
     int surv[32]; // candidates that passed the super-cluster test, in candidate order
+#if NBX_SEARCH_V2
+    float4 sbb[32][2]; // their bounding boxes (lo, hi), so phase B re-reads nothing global
+    float4 ibb[8][2];  // the super-cluster's 8 i-cluster boxes (unshifted)
+#endif
 };
 
 __device__ __forceinline__ float bb_dist2(float4 alo, float4 ahi, float3 v, float4 blo, float4 bhi)
@@ -143,6 +153,24 @@ __device__ __forceinline__ uint2 tile_eval(const SearchArgs& A, const WarpEx& X,
     return ((m.x | m.y) != 0u) ? m : make_uint2(0u, 0u);
 }
 
+// explicit masks of tile (ci, cj) by the whole warp: lane = atom pair (i = lane / 8, j = lane % 8),
+// whose bit is i * 8 + j = lane -- the same bits tile_masks() builds in one lane
+__device__ __forceinline__ uint2 tile_masks_warp(const SearchArgs& A, int ci, int cj, bool exov, bool central,
+                                                 int lane)
+{
+    const int a = 4 * ci + (lane >> 3), b = 8 * cj + (lane & 7);
+    bool ok = A.order_i[a] >= 0 && A.order_j[b] >= 0;
+    if (A.mode == NBX_LIST_LOCAL && central && b <= a) ok = false;
+    bool ex = false;
+    if (ok && exov) {
+        const int ga = A.gid_i[a], gb = A.gid_j[b];
+        const int e1 = A.excl_off[ga + 1];
+        for (int e = A.excl_off[ga]; e < e1; e++) ex |= (A.excl_gid[e] == gb);
+    }
+    const unsigned FULL = 0xffffffffu;
+    return make_uint2(__ballot_sync(FULL, ok && !ex), __ballot_sync(FULL, ok && ex));
+}
+
 template <int MODE>
 #ifndef NBX_SEARCH_MINB
 // 12 CTAs/SM (<= 42 registers, 48 warps): grid + search + prune of a search step 12 M 19.6 ->
@@ -176,6 +204,9 @@ __global__ void __launch_bounds__(SEARCH_THREADS, NBX_SEARCH_MINB) k_search(Sear
             }
         }
     }
+#if NBX_SEARCH_V2
+    if (lane < 16) X.ibb[lane >> 1][lane & 1] = A.bb_ci[2 * (8 * sci) + lane];
+#endif
     __syncwarp();
 
     const float4 slo = A.bb_sci[2 * sci], shi = A.bb_sci[2 * sci + 1];
@@ -264,9 +295,26 @@ __global__ void __launch_bounds__(SEARCH_THREADS, NBX_SEARCH_MINB) k_search(Sear
                     const int ks_o = __shfl_sync(FULL, ks, own);
                     const int cj = 4 * ks_o + (t - base_o);
                     // phase A: one candidate per lane against the super-cluster box
+#if NBX_SEARCH_V2
+                    bool pass = (t < total) && !(A.mode == NBX_LIST_LOCAL && central && cj < 4 * sci);
+                    float4 blo = make_float4(0.f, 0.f, 0.f, 0.f), bhi = blo;
+                    if (pass) {
+                        blo = A.bb_cj[2 * cj];
+                        bhi = A.bb_cj[2 * cj + 1];
+                        pass = blo.w != 0.0f && bb_dist2(slo, shi, v, blo, bhi) < A.rl2;
+                    }
+                    const unsigned S = __ballot_sync(FULL, pass);
+                    if (pass) {
+                        const int r = __popc(S & lt);
+                        X.surv[r] = cj;
+                        X.sbb[r][0] = blo;
+                        X.sbb[r][1] = bhi;
+                    }
+#else
                     const bool pass = (t < total) && sci_test(A, sci, cj, v, central, slo, shi);
                     const unsigned S = __ballot_sync(FULL, pass);
                     if (pass) X.surv[__popc(S & lt)] = cj;
+#endif
                     __syncwarp();
                     const int ns = __popc(S);
                     // phase B: lane = (survivor q0 + lane/8, i-cluster lane%8), 4 survivors per pass
@@ -275,7 +323,31 @@ __global__ void __launch_bounds__(SEARCH_THREADS, NBX_SEARCH_MINB) k_search(Sear
                     for (int q0 = 0; q0 < ns; q0 += 4) {
                         const int q = q0 + sub;
                         const int cjq = (q < ns) ? X.surv[q] : 0;
+#if NBX_SEARCH_V2
+                        uint2 m = make_uint2(0u, 0u);
+                        bool masked = false, exov = false;
+                        if (q < ns) {
+                            const float4 ilo = X.ibb[k][0], ihi = X.ibb[k][1];
+                            const float4 blo = X.sbb[q][0], bhi = X.sbb[q][1];
+                            if (ilo.w != 0.0f && bb_dist2(ilo, ihi, v, blo, bhi) < A.rl2) {
+                                exov = has_partner(X, k, cjq);
+                                masked = ilo.w < 4.0f || blo.w < 8.0f || (central && (cjq >> 2) == sci) || exov;
+                                if (!masked) m = make_uint2(0xffffffffu, 0u);
+                            }
+                        }
+                        // tiles that need explicit masks: one per warp pass, a pair per lane
+                        unsigned mq = __ballot_sync(FULL, masked);
+                        const unsigned xq = __ballot_sync(FULL, exov);
+                        while (mq) {
+                            const int src = __ffs(mq) - 1;
+                            mq &= mq - 1u;
+                            const int tcj = __shfl_sync(FULL, cjq, src);
+                            const uint2 mm = tile_masks_warp(A, 8 * sci + (src & 7), tcj, (xq >> src) & 1u, central, lane);
+                            if (lane == src) m = mm;
+                        }
+#else
                         const uint2 m = (q < ns) ? tile_eval(A, X, sci, k, cjq, v, central) : make_uint2(0u, 0u);
+#endif
                         const bool act = (m.x | m.y) != 0u;
                         const bool need = act && (m.x != 0xffffffffu || m.y != 0u);
                         const unsigned ab = __ballot_sync(FULL, act);

@@ -517,6 +517,7 @@ class DomainDecomposition:
         self._tick("device_repartition")
         chk = torch.tensor([nh, int(over)], dtype=torch.int64, device=dev)
         chk = self._all_reduce(chk).cpu()
+        self._tick("conservation_check")
         if int(chk[1]) or int(chk[0]) != self.sys.natoms:
             # capacity overflow or lost atoms (moved more than one domain): rebuild globally from
             # an all-gather of the home sets (rare; the regions regrow in _peer_map)
@@ -533,10 +534,13 @@ class DomainDecomposition:
         size_l, lo_l, size_n, lo_n = self._grid_boxes()
         eng = self.engine
         eng.grid_build(0, self.x_ext[:self.n_home], self.gid_ext[:self.n_home], lo_l, size_l)
+        self._tick("grid0")
         eng.search(0)
+        self._tick("search0")
         eng.grid_build(1, self.x_ext[self.n_home:], self.gid_ext[self.n_home:], lo_n, size_n)
+        self._tick("grid1")
         eng.search(1)
-        self._tick("grids_searches")
+        self._tick("search1")
         self._peer_owner = B["owner"][:nhalo]
         self._peer_home = B["home"][:nhalo]
         self._peer_shift = B["shift"][:nhalo]

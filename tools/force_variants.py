@@ -12,9 +12,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "scratch", "variants")
 VARIANTS = {
     "base": [],
+    "sv1": ["-DNBX_SEARCH_V2=0"],
     "s10": ["-DNBX_SEARCH_MINB=10"],
-    "s12": ["-DNBX_SEARCH_MINB=12"],
-    "vf3": ["-DNBX_FORCE_MINB_ENERGY=3"],
+    "s8": ["-DNBX_SEARCH_MINB=8"],
 }
 
 
