@@ -75,6 +75,7 @@ enum { SEARCH_COUNT = 0, SEARCH_FILL = 1, SEARCH_SINGLE = 2 };
 struct WarpEx {
     int cj[8][EXMAX];
     int n[8];
+    unsigned long long pbits[8]; // per i-cluster: bit (cj & 63) set for every partner j-cluster
     int surv[32]; // candidates that passed the super-cluster test, in candidate order
 #if NBX_SEARCH_V2
     float4 sbb[32][2]; // their bounding boxes (lo, hi), so phase B re-reads nothing global
@@ -119,11 +120,24 @@ __device__ uint2 tile_masks(const SearchArgs& A, int ci, int cj, bool exov, bool
 
 __device__ __forceinline__ bool has_partner(const WarpEx& X, int k, int cj)
 {
+    // exact negative filter: a j-cluster whose bit is clear is no partner (the list scan below
+    // runs for partners and ~1 in 16 others)
+    if (!((X.pbits[k] >> (cj & 63)) & 1ull)) return false;
     const int n = X.n[k];
     if (n > EXMAX) return true;
     bool hit = false;
     for (int m = 0; m < n; m++) hit |= (X.cj[k][m] == cj);
     return hit;
+}
+
+// bit u of the result = (byte u of b != 0): OR-fold each byte into its bit 0, then gather the
+// four bits with one multiply (the partial products land on distinct bits, no carries)
+__device__ __forceinline__ unsigned byte_any4(unsigned b)
+{
+    b |= b >> 1;
+    b |= b >> 2;
+    b |= b >> 4;
+    return ((b & 0x01010101u) * 0x01020408u) >> 24;
 }
 
 // super-cluster level test of one candidate j-cluster
@@ -189,7 +203,10 @@ __global__ void __launch_bounds__(SEARCH_THREADS, NBX_SEARCH_MINB) k_search(Sear
     const unsigned lt = (1u << lane) - 1u;
 
     // excluded partners of the 32 atoms -> their j-clusters in grid j, per i-cluster
-    if (lane < 8) X.n[lane] = 0;
+    if (lane < 8) {
+        X.n[lane] = 0;
+        X.pbits[lane] = 0ull;
+    }
     __syncwarp();
     {
         const int slot = 32 * sci + lane;
@@ -200,6 +217,7 @@ __global__ void __launch_bounds__(SEARCH_THREADS, NBX_SEARCH_MINB) k_search(Sear
                 if (sp >= 0) {
                     const int pos = atomicAdd(&X.n[lane >> 2], 1);
                     if (pos < EXMAX) X.cj[lane >> 2][pos] = sp >> 3;
+                    atomicOr(&X.pbits[lane >> 2], 1ull << ((sp >> 3) & 63));
                 }
             }
         }
@@ -352,12 +370,8 @@ __global__ void __launch_bounds__(SEARCH_THREADS, NBX_SEARCH_MINB) k_search(Sear
                         const bool need = act && (m.x != 0xffffffffu || m.y != 0u);
                         const unsigned ab = __ballot_sync(FULL, act);
                         const unsigned nb = __ballot_sync(FULL, need);
-                        unsigned am = 0u, pm = 0u; // per-survivor: entry emitted / needs a pool entry
-#pragma unroll
-                        for (int u = 0; u < 4; u++) {
-                            am |= ((ab >> (8 * u)) & 0xffu) ? (1u << u) : 0u;
-                            pm |= ((nb >> (8 * u)) & 0xffu) ? (1u << u) : 0u;
-                        }
+                        // per survivor (byte u of the ballots): entry emitted / needs a pool entry
+                        const unsigned am = byte_any4(ab), pm = byte_any4(nb);
                         if (WRITE && ((am >> sub) & 1u)) {
                             const int cpos = n_cj + __popc(am & sublt);
                             const int ppos = n_pool + __popc(pm & sublt);

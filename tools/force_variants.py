@@ -12,9 +12,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "scratch", "variants")
 VARIANTS = {
     "base": [],
-    "sv1": ["-DNBX_SEARCH_V2=0"],
     "s10": ["-DNBX_SEARCH_MINB=10"],
-    "s8": ["-DNBX_SEARCH_MINB=8"],
 }
 
 
