@@ -666,7 +666,7 @@ __global__ void __launch_bounds__(PRUNE_THREADS, NBX_PRUNE_MINB) k_prune_packed(
     constexpr int W = PRUNE_THREADS / 32;
     __shared__ __align__(16) float s_xj[W][3][32][PRUNE_JS];
     __shared__ float4 s_xi[W][32];
-    __shared__ unsigned s_nm[W][32];
+    __shared__ unsigned s_pass[W][32]; // per pass: the hit ballot (4 lanes per item)
     __shared__ unsigned s_pidx[W][32];
     __shared__ unsigned char s_item[W][256]; // entry << 3 | i-cluster
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -718,7 +718,6 @@ __global__ void __launch_bounds__(PRUNE_THREADS, NBX_PRUNE_MINB) k_prune_packed(
                 mm &= mm - 1u;
             }
         }
-        s_nm[wib][lane] = 0u;
         s_pidx[wib][lane] = my.meta >> 8;
         __syncwarp();
         for (int base = 0; base < total; base += 8) {
@@ -772,10 +771,18 @@ __global__ void __launch_bounds__(PRUNE_THREADS, NBX_PRUNE_MINB) k_prune_packed(
                 hit = r2min < A.rli2;
             }
             const unsigned bits = __ballot_sync(full, hit && m < total);
-            if (ii == 0 && ((bits >> (4 * g)) & 0xfu)) atomicOr(&s_nm[wib][t], 1u << kk);
+            if (lane == 0) s_pass[wib][base >> 3] = bits;
         }
         __syncwarp();
-        const unsigned my_nm = lane < cnt ? s_nm[wib][lane] : 0u;
+        // each entry collects its items' hits (items o .. o + pc - 1, in imask bit order)
+        unsigned my_nm = 0u;
+        {
+            unsigned mm = imask;
+            for (int m = incl - pc; mm; m++) {
+                if ((s_pass[wib][m >> 3] >> (4 * (m & 7))) & 0xfu) my_nm |= mm & (0u - mm);
+                mm &= mm - 1u;
+            }
+        }
         const unsigned keep = __ballot_sync(full, my_nm != 0u);
         if (my_nm) {
             nbx_cj_entry o;
