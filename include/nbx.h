@@ -175,6 +175,17 @@ NBX_API int nbx_grid_build(nbx_ctx* ctx, int grid, int32_t n, const float* x_dev
  * once to size the list (count pass -> exact allocation -> fill pass).                   */
 NBX_API int nbx_search(nbx_ctx* ctx, int list, void* stream);
 
+/* ---- the DD search step's grid builds and searches, overlapped (pipeline.py:329-334, the
+ * decomposed step's pair_search on the home atoms + the nonlocal search) ----------------- *
+ * Same result as nbx_grid_build(0, home...) + nbx_grid_build(1, halo...) + nbx_search(LOCAL)
+ * + nbx_search(NONLOCAL), with the home grid and local list on `stream` and the halo grid
+ * and nonlocal list on `side_stream` (two host waits instead of four; the nonlocal work
+ * fills the SMs the local work leaves idle).  On return `stream` is ordered after all of it. */
+NBX_API int nbx_grid_search_pair(nbx_ctx* ctx, int32_t n_home, const float* x_home_dev, const int32_t* gid_home_dev,
+                                 const float lo_home[3], const float size_home[3], int32_t n_halo,
+                                 const float* x_halo_dev, const int32_t* gid_halo_dev, const float lo_halo[3],
+                                 const float size_halo[3], void* stream, void* side_stream);
+
 /* ---- X buffer op (folded into NBNXM_* in the reference model, pipeline.py:231) ------- *
  * Copy user-order coordinates of grid `grid` into the cluster-ordered xyzq buffer, with
  * the wrap shifts fixed at the last grid build.                                          */

@@ -235,12 +235,12 @@ NBX_API int nbx_destroy(nbx_ctx* ctx)
         G.key.release(); G.key_out.release(); G.val.release(); G.val_out.release(); G.xw.release();
         G.order.release(); G.gid.release(); G.type.release(); G.xq.release(); G.wrapk.release();
         G.f.release(); G.bb_ci.release(); G.bb_cj.release(); G.bb_sci.release();
-        G.slotmap.release(); G.islot.release(); G.bb_col.release(); G.tmp.release();
+        G.slotmap.release(); G.islot.release(); G.bb_col.release(); G.tmp.release(); G.padded.release();
         List& L = ctx->list[g];
         L.sci.release(); L.sci_in.release(); L.cj.release(); L.cj_in.release(); L.pool.release();
         L.counts.release(); L.offsets.release(); L.totals.release(); L.tmp.release();
         L.len_key.release(); L.len_key_out.release(); L.order_in.release(); L.order.release(); L.sort_tmp.release();
-        L.flags.release(); L.tsci.release(); L.tcj.release(); L.tpool.release();
+        L.flags.release(); L.tsci.release(); L.tcj.release(); L.tpool.release(); L.pair_count.release();
     }
     ctx->q_g.release(); ctx->type_g.release(); ctx->excl_off_g.release(); ctx->excl_gid_g.release();
     ctx->c6c12s.release(); ctx->acc.release(); ctx->sumq2.release(); ctx->counter.release();
@@ -249,6 +249,9 @@ NBX_API int nbx_destroy(nbx_ctx* ctx)
     for (auto& g : ctx->full_graphs) cudaGraphExecDestroy(g.exec);
     peer_release(ctx);
     if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
+    if (ctx->h_pin) cudaFreeHost(ctx->h_pin);
+    for (cudaEvent_t e : ctx->ev_pair)
+        if (e) cudaEventDestroy(e);
     delete ctx;
     return NBX_OK;
     NBX_GUARD_END
@@ -402,6 +405,48 @@ NBX_API int nbx_search(nbx_ctx* ctx, int list, void* stream)
     if (!ctx->grid[0].built || (list == 1 && !ctx->grid[1].built))
         return fail(NBX_EINVAL, "build the grid(s) first");
     search(ctx, list, (cudaStream_t)stream);
+    ctx->epoch++;
+    return NBX_OK;
+    NBX_GUARD_END
+}
+
+NBX_API int nbx_grid_search_pair(nbx_ctx* ctx, int32_t n_home, const float* x_home, const int32_t* gid_home,
+                                 const float lo_home[3], const float size_home[3], int32_t n_halo,
+                                 const float* x_halo, const int32_t* gid_halo, const float lo_halo[3],
+                                 const float size_halo[3], void* stream, void* side_stream)
+{
+    NBX_GUARD_BEGIN
+    NBX_CHECK_CTX(ctx);
+    if (!ctx->have_topology || !ctx->have_box) return fail(NBX_EINVAL, "set topology and box first");
+    if (n_home < 0 || n_halo < 0 || (n_home > 0 && !x_home) || (n_halo > 0 && !x_halo) || !lo_home ||
+        !size_home || !lo_halo || !size_halo)
+        return fail(NBX_EINVAL, "bad grid arguments");
+    if (gid_home == nullptr && n_home != ctx->natoms_global)
+        return fail(NBX_EINVAL, "identity gid requires n == natoms_global");
+    for (int d = 0; d < 3; d++)
+        if (!(size_home[d] > 0.0f) || !(size_halo[d] > 0.0f))
+            return fail(NBX_EINVAL, "grid region size must be positive");
+    cudaStream_t st0 = (cudaStream_t)stream, st1 = (cudaStream_t)side_stream;
+    if (st0 == st1) return fail(NBX_EINVAL, "side_stream must differ from stream");
+    if (!ctx->ev_pair[0]) {
+        NBX_CUDA(cudaEventCreateWithFlags(&ctx->ev_pair[0], cudaEventDisableTiming));
+        NBX_CUDA(cudaEventCreateWithFlags(&ctx->ev_pair[1], cudaEventDisableTiming));
+    }
+    ctx->list[0].built = false;
+    ctx->list[1].built = false;
+    // the inputs were produced in `stream` order: the side stream starts after them
+    NBX_CUDA(cudaEventRecord(ctx->ev_pair[0], st0));
+    NBX_CUDA(cudaStreamWaitEvent(st1, ctx->ev_pair[0], 0));
+    const GridReq r[2] = {{n_home, x_home, gid_home, lo_home, size_home},
+                          {n_halo, x_halo, gid_halo, lo_halo, size_halo}};
+    grid_build_pair(ctx, r, st0, st1);
+    ctx->epoch++;
+    // the nonlocal list's i grid is grid 0
+    NBX_CUDA(cudaEventRecord(ctx->ev_pair[0], st0));
+    NBX_CUDA(cudaStreamWaitEvent(st1, ctx->ev_pair[0], 0));
+    search_pair(ctx, st0, st1);
+    NBX_CUDA(cudaEventRecord(ctx->ev_pair[1], st1));
+    NBX_CUDA(cudaStreamWaitEvent(st0, ctx->ev_pair[1], 0));
     ctx->epoch++;
     return NBX_OK;
     NBX_GUARD_END

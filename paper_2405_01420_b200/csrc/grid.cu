@@ -23,6 +23,13 @@ struct BinArgs {
     int ncx, ncy;
 };
 
+// what grid_end needs from grid_begin
+struct GridStage {
+    BinArgs B;
+    const int* gid = nullptr;
+    int* h = nullptr; // pinned: [0] padded slot count
+};
+
 __device__ __forceinline__ float wrap_k(float x, float invL, int pbc)
 {
     return pbc ? floorf(__fmul_rn(x, invL)) : 0.0f;
@@ -264,8 +271,13 @@ static int bits_for(int v)
     return b;
 }
 
-void grid_build(nbx_ctx* ctx, int g, int n, const float* x, const int* gid, const float lo[3],
-                const float size[3], cudaStream_t st)
+// grid build in two halves around the one host read it needs (the padded slot count, which
+// sizes every later buffer and launch): grid_begin enqueues binning, the column sort and the
+// scans plus an async read into pinned host memory; grid_end, after the caller has waited,
+// enqueues the slab fill and the bounding boxes.  grid_build = begin + wait + end;
+// grid_build_pair overlaps two grids (DD: home + halo) on two streams with one wait.
+static void grid_begin(nbx_ctx* ctx, int g, int n, const float* x, const int* gid, const float lo[3],
+                const float size[3], cudaStream_t st, GridStage& S)
 {
     Grid& G = ctx->grid[g];
     G.n = n;
@@ -316,9 +328,19 @@ void grid_build(nbx_ctx* ctx, int g, int n, const float* x, const int* gid, cons
     NBX_CUDA(cub::DeviceScan::ExclusiveSum(G.tmp.p, tb1, padded, G.col_start.p, G.ncol + 1, st));
     NBX_CUDA(cub::DeviceScan::ExclusiveSum(G.tmp.p, tb2, G.col_count.p, G.col_astart.p, G.ncol + 1, st));
     ctx->launches += 2;
-    int nslots = 0;
-    NBX_CUDA(cudaMemcpyAsync(&nslots, G.col_start.p + G.ncol, sizeof(int), cudaMemcpyDeviceToHost, st));
-    NBX_CUDA(cudaStreamSynchronize(st));
+    S.B = B;
+    S.gid = gid;
+    S.h = host_pin(ctx) + 4 * g; // [0]: padded slot count
+    NBX_CUDA(cudaMemcpyAsync(S.h, G.col_start.p + G.ncol, sizeof(int), cudaMemcpyDeviceToHost, st));
+}
+
+static void grid_end(nbx_ctx* ctx, int g, cudaStream_t st, const GridStage& S)
+{
+    Grid& G = ctx->grid[g];
+    const BinArgs& B = S.B;
+    const int* gid = S.gid;
+    const int n = G.n, nn = n > 0 ? n : 1;
+    const int nslots = S.h[0];
     G.nslots = nslots;
     G.nsci = nslots / 32;
     const int ns = nslots > 0 ? nslots : 32;
@@ -372,6 +394,26 @@ void grid_build(nbx_ctx* ctx, int g, int n, const float* x, const int* gid, cons
     ctx->launches++;
     NBX_CUDA(cudaGetLastError());
     G.built = true;
+}
+
+void grid_build(nbx_ctx* ctx, int g, int n, const float* x, const int* gid, const float lo[3],
+                const float size[3], cudaStream_t st)
+{
+    GridStage S;
+    grid_begin(ctx, g, n, x, gid, lo, size, st, S);
+    NBX_CUDA(cudaStreamSynchronize(st));
+    grid_end(ctx, g, st, S);
+}
+
+void grid_build_pair(nbx_ctx* ctx, const GridReq r[2], cudaStream_t st0, cudaStream_t st1)
+{
+    GridStage S0, S1;
+    grid_begin(ctx, 0, r[0].n, r[0].x, r[0].gid, r[0].lo, r[0].size, st0, S0);
+    grid_begin(ctx, 1, r[1].n, r[1].x, r[1].gid, r[1].lo, r[1].size, st1, S1);
+    NBX_CUDA(cudaStreamSynchronize(st0));
+    NBX_CUDA(cudaStreamSynchronize(st1));
+    grid_end(ctx, 0, st0, S0);
+    grid_end(ctx, 1, st1, S1);
 }
 
 } // namespace nbx

@@ -188,7 +188,19 @@ struct nbx_ctx {
     };
     std::vector<FullGraph> full_graphs;
     cudaStream_t cap_stream = nullptr;
+    // pinned host words for the search step's size reads (async copies; grid g at [4 g],
+    // list l at [8 + 8 l])
+    int* h_pin = nullptr;
+    cudaEvent_t ev_pair[2] = {nullptr, nullptr}; // nbx_grid_search_pair stream ordering
 };
+
+namespace nbx {
+inline int* host_pin(nbx_ctx* ctx)
+{
+    if (!ctx->h_pin) NBX_CUDA(cudaMallocHost((void**)&ctx->h_pin, 32 * sizeof(int)));
+    return ctx->h_pin;
+}
+} // namespace nbx
 
 // PME context (row f4; pme.cu)
 struct nbx_pme {
@@ -240,6 +252,18 @@ __device__ __forceinline__ float3 shift_vec(int s, float3 box)
 }
 
 // ---- launchers (defined in the .cu files) -----------------------------------------------
+struct GridReq {
+    int n;
+    const float* x;
+    const int* gid;
+    const float* lo;
+    const float* size;
+};
+// grids 0 and 1 built concurrently on st0 / st1 with one host wait (DD search steps)
+void grid_build_pair(nbx_ctx* ctx, const GridReq r[2], cudaStream_t st0, cudaStream_t st1);
+// lists 0 and 1 searched concurrently on st0 / st1 with one host wait; st1 must already be
+// ordered after grid 0's build (list 1's i grid), st0 is not ordered after st1 on return
+void search_pair(nbx_ctx* ctx, cudaStream_t st0, cudaStream_t st1);
 void grid_build(nbx_ctx* ctx, int g, int n, const float* x, const int* gid, const float lo[3],
                 const float size[3], cudaStream_t st);
 void search(nbx_ctx* ctx, int l, cudaStream_t st);

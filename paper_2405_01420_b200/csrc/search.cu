@@ -1038,7 +1038,17 @@ void prune(nbx_ctx* ctx, int l, int part, int nparts, cudaStream_t st)
     if (L.use_order) sort_entries(ctx, L, st);
 }
 
-void search(nbx_ctx* ctx, int l, cudaStream_t st)
+// search in two halves around the host read of the list sizes (search_begin: kernels, scans
+// and an async read into pinned memory; search_end, after the caller's wait: allocation,
+// compaction or fill, prune), so search_pair can overlap the local and nonlocal lists
+struct SearchStage {
+    SearchArgs A;
+    bool single = false;
+    int blocks = 0, nsci = 0;
+    int* h = nullptr; // pinned: [0..2] entry / cj / pool totals, [3..6] flags
+};
+
+static void search_begin(nbx_ctx* ctx, int l, cudaStream_t st, SearchStage& S)
 {
     List& L = ctx->list[l];
     L.mode = l;
@@ -1116,12 +1126,25 @@ void search(nbx_ctx* ctx, int l, cudaStream_t st)
                                                L.offsets.p + k * (nsci + 1), nsci + 1, st));
         ctx->launches++;
     }
-    int tot[3], fl[4];
+    S.A = A;
+    S.single = single;
+    S.blocks = blocks;
+    S.nsci = nsci;
+    S.h = host_pin(ctx) + 8 + 8 * l;
     for (int k = 0; k < 3; k++)
-        NBX_CUDA(cudaMemcpyAsync(&tot[k], L.offsets.p + k * (nsci + 1) + nsci, sizeof(int),
+        NBX_CUDA(cudaMemcpyAsync(S.h + k, L.offsets.p + k * (nsci + 1) + nsci, sizeof(int),
                                  cudaMemcpyDeviceToHost, st));
-    NBX_CUDA(cudaMemcpyAsync(fl, L.flags.p, sizeof(fl), cudaMemcpyDeviceToHost, st));
-    NBX_CUDA(cudaStreamSynchronize(st));
+    NBX_CUDA(cudaMemcpyAsync(S.h + 3, L.flags.p, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
+}
+
+static void search_end(nbx_ctx* ctx, int l, cudaStream_t st, SearchStage& S)
+{
+    List& L = ctx->list[l];
+    SearchArgs& A = S.A;
+    const bool single = S.single;
+    const int blocks = S.blocks, nsci = S.nsci;
+    const int* tot = S.h;
+    const int* fl = S.h + 3;
     L.n_sci = tot[0];
     L.n_cj = tot[1];
     L.n_pool = (int64_t)tot[2] + 1;
@@ -1165,6 +1188,25 @@ void search(nbx_ctx* ctx, int l, cudaStream_t st)
     }
     L.built = true;
     prune(ctx, l, 0, 1, st);
+}
+
+void search(nbx_ctx* ctx, int l, cudaStream_t st)
+{
+    SearchStage S;
+    search_begin(ctx, l, st, S);
+    NBX_CUDA(cudaStreamSynchronize(st));
+    search_end(ctx, l, st, S);
+}
+
+void search_pair(nbx_ctx* ctx, cudaStream_t st0, cudaStream_t st1)
+{
+    SearchStage S0, S1;
+    search_begin(ctx, 0, st0, S0);
+    search_begin(ctx, 1, st1, S1);
+    NBX_CUDA(cudaStreamSynchronize(st0));
+    NBX_CUDA(cudaStreamSynchronize(st1));
+    search_end(ctx, 0, st0, S0);
+    search_end(ctx, 1, st1, S1);
 }
 
 } // namespace nbx

@@ -100,6 +100,17 @@ class NbxEngine:
     def search(self, lst):
         self.nbx.check(self.nbx.lib().nbx_search(self.ctx.h, lst, self._st()))
 
+    def grid_search_pair(self, x_home, gid_home, lo_l, size_l, x_halo, gid_halo, lo_n, size_n, side_stream):
+        """Both grids and both lists of a DD search step, the halo half on side_stream."""
+        nbx = self.nbx
+        a = [np.ascontiguousarray(v, np.float32) for v in (lo_l, size_l, lo_n, size_n)]
+        nh, nn = int(x_home.shape[0]), int(x_halo.shape[0])
+        nbx.check(nbx.lib().nbx_grid_search_pair(
+            self.ctx.h, nh, nbx._dev_ptr(x_home) if nh else None, nbx._dev_ptr(gid_home) if nh else None,
+            nbx._ptr(a[0]), nbx._ptr(a[1]), nn, nbx._dev_ptr(x_halo) if nn else None,
+            nbx._dev_ptr(gid_halo) if nn else None, nbx._ptr(a[2]), nbx._ptr(a[3]), self._st(),
+            self._st(side_stream)))
+
     def put_x(self, g, x, stream=None):
         if x.shape[0]:
             self.nbx.check(self.nbx.lib().nbx_put_x(self.ctx.h, g, self.nbx._dev_ptr(x), self._st(stream)))
@@ -252,6 +263,7 @@ class DomainDecomposition:
         # p2p steps: halo gather + nonlocal force on a side stream (NBX_DD_OVERLAP=0 disables)
         self.overlap_nonlocal = os.environ.get("NBX_DD_OVERLAP", "1") != "0"
         self._side = None
+        self._ev_x = self._ev_nl = None
         self._peer_cap = 0
         self.rseq = 0             # device repartitions so far (peer-path search steps)
         self._rp = None           # device-repartition output buffers (capacity-sized)
@@ -431,14 +443,23 @@ class DomainDecomposition:
         lo_n = np.array([lo[d] - self.rl if self.dims[d] > 1 else 0.0 for d in range(3)], np.float32)
         eng = self.engine
         self._tick("buffers")
-        eng.grid_build(0, self.x_ext[:self.n_home], self.gid_ext[:self.n_home], lo_l, size_l)
-        self._tick("grid0")
-        eng.search(0)
-        self._tick("search0")
-        eng.grid_build(1, self.x_ext[self.n_home:], self.gid_ext[self.n_home:], lo_n, size_n)
-        self._tick("grid1")
-        eng.search(1)
-        self._tick("search1")
+        if hasattr(eng, "grid_search_pair") and os.environ.get("NBX_DD_PAIR_SEARCH", "1") != "0":
+            # home grid + local list on this stream, halo grid + nonlocal list on the side
+            # stream, overlapped (nbx_grid_search_pair)
+            if self._side is None:
+                self._side = torch.cuda.Stream(device=self.device)
+            eng.grid_search_pair(self.x_ext[:self.n_home], self.gid_ext[:self.n_home], lo_l, size_l,
+                                 self.x_ext[self.n_home:], self.gid_ext[self.n_home:], lo_n, size_n, self._side)
+            self._tick("grids_searches")
+        else:
+            eng.grid_build(0, self.x_ext[:self.n_home], self.gid_ext[:self.n_home], lo_l, size_l)
+            self._tick("grid0")
+            eng.search(0)
+            self._tick("search0")
+            eng.grid_build(1, self.x_ext[self.n_home:], self.gid_ext[self.n_home:], lo_n, size_n)
+            self._tick("grid1")
+            eng.search(1)
+            self._tick("search1")
         if self.halo == "p2p":
             self._peer_map()
             self._tick("peer_map")
@@ -533,14 +554,23 @@ class DomainDecomposition:
         self.pulses = []  # the message-passing halo plan is not built on this path
         size_l, lo_l, size_n, lo_n = self._grid_boxes()
         eng = self.engine
-        eng.grid_build(0, self.x_ext[:self.n_home], self.gid_ext[:self.n_home], lo_l, size_l)
-        self._tick("grid0")
-        eng.search(0)
-        self._tick("search0")
-        eng.grid_build(1, self.x_ext[self.n_home:], self.gid_ext[self.n_home:], lo_n, size_n)
-        self._tick("grid1")
-        eng.search(1)
-        self._tick("search1")
+        if hasattr(eng, "grid_search_pair") and os.environ.get("NBX_DD_PAIR_SEARCH", "1") != "0":
+            # home grid + local list on this stream, halo grid + nonlocal list on the side
+            # stream, overlapped (nbx_grid_search_pair)
+            if self._side is None:
+                self._side = torch.cuda.Stream(device=self.device)
+            eng.grid_search_pair(self.x_ext[:self.n_home], self.gid_ext[:self.n_home], lo_l, size_l,
+                                 self.x_ext[self.n_home:], self.gid_ext[self.n_home:], lo_n, size_n, self._side)
+            self._tick("grids_searches")
+        else:
+            eng.grid_build(0, self.x_ext[:self.n_home], self.gid_ext[:self.n_home], lo_l, size_l)
+            self._tick("grid0")
+            eng.search(0)
+            self._tick("search0")
+            eng.grid_build(1, self.x_ext[self.n_home:], self.gid_ext[self.n_home:], lo_n, size_n)
+            self._tick("grid1")
+            eng.search(1)
+            self._tick("search1")
         self._peer_owner = B["owner"][:nhalo]
         self._peer_home = B["home"][:nhalo]
         self._peer_shift = B["shift"][:nhalo]
@@ -732,6 +762,7 @@ class DomainDecomposition:
             main = torch.cuda.current_stream()
             if self._side is None:
                 self._side = torch.cuda.Stream(device=self.device)
+            if self._ev_x is None:
                 self._ev_x = torch.cuda.Event()
                 self._ev_nl = torch.cuda.Event()
             self._ev_x.record(main)

@@ -71,7 +71,7 @@ POOL_DTYPE = np.dtype(("<u4", (8, 2)))
 
 # every symbol include/nbx.h declares (checked by tests/test_capi.py)
 EXPORTS = ["nbx_last_error", "nbx_version", "nbx_derive_consts", "nbx_ewald_table", "nbx_create", "nbx_destroy",
-           "nbx_set_topology", "nbx_set_box", "nbx_grid_build", "nbx_search", "nbx_put_x",
+           "nbx_set_topology", "nbx_set_box", "nbx_grid_build", "nbx_search", "nbx_grid_search_pair", "nbx_put_x",
            "nbx_prune", "nbx_force", "nbx_get_f", "nbx_step_graph", "nbx_energies", "nbx_clear_energies",
            "nbx_grid_info_get", "nbx_grid_export", "nbx_list_sizes_get", "nbx_list_export",
            "nbx_count_pairs", "nbx_fma_peak", "nbx_launch_count", "nbx_alloc_count", "nbx_halo_pack_x", "nbx_halo_unpack_add_f",
@@ -103,6 +103,7 @@ def lib():
         L.nbx_set_box.argtypes = [vp, vp, vp]
         L.nbx_grid_build.argtypes = [vp, C.c_int, i32, vp, vp, vp, vp, vp]
         L.nbx_search.argtypes = [vp, C.c_int, vp]
+        L.nbx_grid_search_pair.argtypes = [vp, i32, vp, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp]
         L.nbx_put_x.argtypes = [vp, C.c_int, vp, vp]
         L.nbx_prune.argtypes = [vp, C.c_int, C.c_int, C.c_int, vp]
         L.nbx_force.argtypes = [vp, C.c_int, u32, vp]
