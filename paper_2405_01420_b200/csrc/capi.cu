@@ -216,6 +216,7 @@ NBX_API int nbx_create(int device, const nbx_params* p, nbx_ctx** out)
     // nbx_internal.cuh) -- on for the mid-size lists whose tail it shortens, off for the 12 M
     // box (longest-first costs L2 locality there, +5 %) and for tiny lists; DESIGN.md section 5
     if (const char* pk = std::getenv("NBX_PRUNE_KERNEL")) ctx->prune_kernel = std::atoi(pk);
+    if (const char* ps = std::getenv("NBX_PRUNE_SPLIT")) ctx->prune_split = std::atoi(ps);
     if (const char* eo = std::getenv("NBX_ENTRY_ORDER")) ctx->entry_order = std::atoi(eo);
     if (const char* fs = std::getenv("NBX_FORCE_SPLIT")) ctx->force_split = std::atoi(fs);
     *out = ctx;
@@ -241,6 +242,7 @@ NBX_API int nbx_destroy(nbx_ctx* ctx)
         L.counts.release(); L.offsets.release(); L.totals.release(); L.tmp.release();
         L.len_key.release(); L.len_key_out.release(); L.order_in.release(); L.order.release(); L.sort_tmp.release();
         L.flags.release(); L.tsci.release(); L.tcj.release(); L.tpool.release(); L.pair_count.release();
+        L.prune_tmp.release(); L.prune_kept.release();
     }
     ctx->q_g.release(); ctx->type_g.release(); ctx->excl_off_g.release(); ctx->excl_gid_g.release();
     ctx->c6c12s.release(); ctx->acc.release(); ctx->sumq2.release(); ctx->counter.release();

@@ -107,6 +107,9 @@ struct List {
     DBuf<nbx_cj_entry> tcj;
     DBuf<nbx_mask_pool_entry> tpool;
     DBuf<char> tmp;
+    int prune_chunks = 0;            // split prune: 32-entry chunks of the longest sci (0: off)
+    DBuf<nbx_cj_entry> prune_tmp;    // split prune: per-chunk compacted entries [n_cj]
+    DBuf<int> prune_kept;            // split prune: kept count per (entry, chunk)
 };
 
 struct Peer; // peer.cu: NVLink peer-memory halo state (DD, row e)
@@ -146,6 +149,7 @@ struct nbx_ctx {
     nbx::DBuf<int> counter;   // work counters [8]
     int64_t launches = 0;
     int force_split = 0; // > 0: fixed work items per sci entry (env NBX_FORCE_SPLIT), 0: auto
+    int prune_split = -1; // split prune for short lists: -1 auto, 0 off, 1 on (env NBX_PRUNE_SPLIT)
     int prune_kernel = 2; // 0: k_prune (lane per cj entry), 1: k_prune_lanes (lane per i atom), 2: k_prune_packed (compacted tiles, FP32x2); env NBX_PRUNE_KERNEL
     // row f2, force-kernel work order: 0 = list order (spatially coherent), 1 = longest entry
     // first (sorted after every prune), -1 = auto (default): longest first for lists of

@@ -661,128 +661,148 @@ __global__ void __launch_bounds__(PRUNE_THREADS) k_prune_lanes(PruneArgs A)
 #endif
 constexpr int PRUNE_JS = NBX_PRUNE_JS;
 
+// per-warp shared staging of the packed prune
+struct PruneWarpSmem {
+    float xj[3][32][PRUNE_JS];
+    float4 xi[32];
+    unsigned pass[32]; // per pass: the hit ballot (4 lanes per item)
+    unsigned pidx[32];
+    unsigned char item[256]; // entry << 3 | i-cluster
+};
+
+// i atoms of sci entry se (+ its shift) into the warp's staging
+__device__ __forceinline__ void prune_stage_i(const PruneArgs& A, const nbx_sci_entry& se, PruneWarpSmem& S, int lane)
+{
+    const float3 v = shift_vec(se.shift, A.box);
+    const float4 t0 = A.xq_i[32 * se.sci + lane];
+    S.xi[lane] = make_float4(__fadd_rn(t0.x, v.x), __fadd_rn(t0.y, v.y), __fadd_rn(t0.z, v.z), 0.f);
+}
+
+// one chunk of up to 32 cj entries starting at c0 of an entry ending at cj_end: returns this
+// lane's entry (my) and its new interaction mask (0: dropped)
+__device__ __forceinline__ unsigned prune_chunk_packed(const PruneArgs& A, PruneWarpSmem& S, int lane, int c0,
+                                                       int cj_end, nbx_cj_entry& my)
+{
+    const unsigned full = 0xffffffffu;
+    const int g = lane >> 2, ii = lane & 3;
+    const int cnt = min(32, cj_end - c0);
+    my.cj = 0;
+    my.meta = 0u;
+    if (lane < cnt) my = A.cj[c0 + lane];
+    __syncwarp();
+    for (int r = 0; r < 8 && 4 * r < cnt; r++) {
+        const int t = 4 * r + (lane >> 3);
+        const int cjt = __shfl_sync(full, my.cj, t);
+        if (t < cnt) {
+            const int j = lane & 7;
+            const float4 b = A.xq_j[8 * cjt + j];
+            S.xj[0][t][j] = b.x;
+            S.xj[1][t][j] = b.y;
+            S.xj[2][t][j] = b.z;
+        }
+    }
+    // item table: exclusive scan of the entries' active-tile counts
+    const unsigned imask = my.meta & 0xffu;
+    const int pc = __popc(imask);
+    int incl = pc;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int y = __shfl_up_sync(full, incl, d);
+        if (lane >= d) incl += y;
+    }
+    const int total = __shfl_sync(full, incl, 31);
+    {
+        unsigned mm = imask;
+        int o = incl - pc;
+        while (mm) {
+            S.item[o++] = (unsigned char)((lane << 3) | (__ffs(mm) - 1));
+            mm &= mm - 1u;
+        }
+    }
+    S.pidx[lane] = my.meta >> 8;
+    __syncwarp();
+    for (int base = 0; base < total; base += 8) {
+        const int m = base + g;
+        const unsigned it = m < total ? S.item[m] : 0u;
+        const int t = it >> 3, kk = it & 7;
+        const float4 a = S.xi[4 * kk + ii];
+        const unsigned pidx = S.pidx[t];
+        const float* xs = S.xj[0][t];
+        const float* ys = S.xj[1][t];
+        const float* zs = S.xj[2][t];
+        bool hit = false;
+        if (!__any_sync(full, pidx != 0u)) {
+            const f2x AX = bc(a.x), AY = bc(a.y), AZ = bc(a.z);
+            float r2min = 0.f;
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const ulonglong2 X = *reinterpret_cast<const ulonglong2*>(xs + 4 * h);
+                const ulonglong2 Y = *reinterpret_cast<const ulonglong2*>(ys + 4 * h);
+                const ulonglong2 Z = *reinterpret_cast<const ulonglong2*>(zs + 4 * h);
+                const f2x DX0 = sub2(X.x, AX), DY0 = sub2(Y.x, AY), DZ0 = sub2(Z.x, AZ);
+                const f2x DX1 = sub2(X.y, AX), DY1 = sub2(Y.y, AY), DZ1 = sub2(Z.y, AZ);
+                const float2 R0 = upk(fma2(DZ0, DZ0, fma2(DY0, DY0, mul2(DX0, DX0))));
+                const float2 R1 = upk(fma2(DZ1, DZ1, fma2(DY1, DY1, mul2(DX1, DX1))));
+                const float m4 = fminf(fminf(R0.x, R0.y), fminf(R1.x, R1.y));
+                r2min = h ? fminf(r2min, m4) : m4;
+            }
+            hit = r2min < A.rli2;
+        } else {
+            // a pass holding an excluded (pool) tile: the same packed r^2, with masked
+            // pairs' r^2 replaced by +inf before the minimum
+            unsigned row = 0xffu;
+            if (pidx) row = ((A.pool[pidx].m[kk][0] | A.pool[pidx].m[kk][1]) >> (8 * ii)) & 0xffu;
+            const f2x AX = bc(a.x), AY = bc(a.y), AZ = bc(a.z);
+            float r2min = 0.f;
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const ulonglong2 X = *reinterpret_cast<const ulonglong2*>(xs + 4 * h);
+                const ulonglong2 Y = *reinterpret_cast<const ulonglong2*>(ys + 4 * h);
+                const ulonglong2 Z = *reinterpret_cast<const ulonglong2*>(zs + 4 * h);
+                const f2x DX0 = sub2(X.x, AX), DY0 = sub2(Y.x, AY), DZ0 = sub2(Z.x, AZ);
+                const f2x DX1 = sub2(X.y, AX), DY1 = sub2(Y.y, AY), DZ1 = sub2(Z.y, AZ);
+                const float2 R0 = upk(fma2(DZ0, DZ0, fma2(DY0, DY0, mul2(DX0, DX0))));
+                const float2 R1 = upk(fma2(DZ1, DZ1, fma2(DY1, DY1, mul2(DX1, DX1))));
+                const unsigned rb = row >> (4 * h);
+                const float inf = __int_as_float(0x7f800000);
+                const float m4 = fminf(fminf((rb & 1u) ? R0.x : inf, (rb & 2u) ? R0.y : inf),
+                                       fminf((rb & 4u) ? R1.x : inf, (rb & 8u) ? R1.y : inf));
+                r2min = h ? fminf(r2min, m4) : m4;
+            }
+            hit = r2min < A.rli2;
+        }
+        const unsigned bits = __ballot_sync(full, hit && m < total);
+        if (lane == 0) S.pass[base >> 3] = bits;
+    }
+    __syncwarp();
+    // each entry collects its items' hits (items o .. o + pc - 1, in imask bit order)
+    unsigned my_nm = 0u;
+    {
+        unsigned mm = imask;
+        for (int m = incl - pc; mm; m++) {
+            if ((S.pass[m >> 3] >> (4 * (m & 7))) & 0xfu) my_nm |= mm & (0u - mm);
+            mm &= mm - 1u;
+        }
+    }
+    return lane < cnt ? my_nm : 0u;
+}
+
 __global__ void __launch_bounds__(PRUNE_THREADS, NBX_PRUNE_MINB) k_prune_packed(PruneArgs A)
 {
     constexpr int W = PRUNE_THREADS / 32;
-    __shared__ __align__(16) float s_xj[W][3][32][PRUNE_JS];
-    __shared__ float4 s_xi[W][32];
-    __shared__ unsigned s_pass[W][32]; // per pass: the hit ballot (4 lanes per item)
-    __shared__ unsigned s_pidx[W][32];
-    __shared__ unsigned char s_item[W][256]; // entry << 3 | i-cluster
+    __shared__ __align__(16) PruneWarpSmem s_w[W];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int e = A.part + A.nparts * w;
     if (e >= A.n_sci) return;
     const unsigned full = 0xffffffffu, lt = (1u << lane) - 1u;
+    PruneWarpSmem& S = s_w[wib];
     const nbx_sci_entry se = A.sci[e];
-    {
-        const float3 v = shift_vec(se.shift, A.box);
-        const float4 t0 = A.xq_i[32 * se.sci + lane];
-        s_xi[wib][lane] = make_float4(__fadd_rn(t0.x, v.x), __fadd_rn(t0.y, v.y), __fadd_rn(t0.z, v.z), 0.f);
-    }
-    const int g = lane >> 2, ii = lane & 3;
+    prune_stage_i(A, se, S, lane);
     int kept = 0;
     for (int c0 = se.cj_start; c0 < se.cj_end; c0 += 32) {
-        const int cnt = min(32, se.cj_end - c0);
         nbx_cj_entry my;
-        my.cj = 0;
-        my.meta = 0u;
-        if (lane < cnt) my = A.cj[c0 + lane];
-        __syncwarp();
-        for (int r = 0; r < 8 && 4 * r < cnt; r++) {
-            const int t = 4 * r + (lane >> 3);
-            const int cjt = __shfl_sync(full, my.cj, t);
-            if (t < cnt) {
-                const int j = lane & 7;
-                const float4 b = A.xq_j[8 * cjt + j];
-                s_xj[wib][0][t][j] = b.x;
-                s_xj[wib][1][t][j] = b.y;
-                s_xj[wib][2][t][j] = b.z;
-            }
-        }
-        // item table: exclusive scan of the entries' active-tile counts
-        const unsigned imask = my.meta & 0xffu;
-        const int pc = __popc(imask);
-        int incl = pc;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const int y = __shfl_up_sync(full, incl, d);
-            if (lane >= d) incl += y;
-        }
-        const int total = __shfl_sync(full, incl, 31);
-        {
-            unsigned mm = imask;
-            int o = incl - pc;
-            while (mm) {
-                s_item[wib][o++] = (unsigned char)((lane << 3) | (__ffs(mm) - 1));
-                mm &= mm - 1u;
-            }
-        }
-        s_pidx[wib][lane] = my.meta >> 8;
-        __syncwarp();
-        for (int base = 0; base < total; base += 8) {
-            const int m = base + g;
-            const unsigned it = m < total ? s_item[wib][m] : 0u;
-            const int t = it >> 3, kk = it & 7;
-            const float4 a = s_xi[wib][4 * kk + ii];
-            const unsigned pidx = s_pidx[wib][t];
-            const float* xs = s_xj[wib][0][t];
-            const float* ys = s_xj[wib][1][t];
-            const float* zs = s_xj[wib][2][t];
-            bool hit = false;
-            if (!__any_sync(full, pidx != 0u)) {
-                const f2x AX = bc(a.x), AY = bc(a.y), AZ = bc(a.z);
-                float r2min = 0.f;
-#pragma unroll
-                for (int h = 0; h < 2; h++) {
-                    const ulonglong2 X = *reinterpret_cast<const ulonglong2*>(xs + 4 * h);
-                    const ulonglong2 Y = *reinterpret_cast<const ulonglong2*>(ys + 4 * h);
-                    const ulonglong2 Z = *reinterpret_cast<const ulonglong2*>(zs + 4 * h);
-                    const f2x DX0 = sub2(X.x, AX), DY0 = sub2(Y.x, AY), DZ0 = sub2(Z.x, AZ);
-                    const f2x DX1 = sub2(X.y, AX), DY1 = sub2(Y.y, AY), DZ1 = sub2(Z.y, AZ);
-                    const float2 R0 = upk(fma2(DZ0, DZ0, fma2(DY0, DY0, mul2(DX0, DX0))));
-                    const float2 R1 = upk(fma2(DZ1, DZ1, fma2(DY1, DY1, mul2(DX1, DX1))));
-                    const float m4 = fminf(fminf(R0.x, R0.y), fminf(R1.x, R1.y));
-                    r2min = h ? fminf(r2min, m4) : m4;
-                }
-                hit = r2min < A.rli2;
-            } else {
-                // a pass holding an excluded (pool) tile: the same packed r^2, with masked
-                // pairs' r^2 replaced by +inf before the minimum
-                unsigned row = 0xffu;
-                if (pidx) row = ((A.pool[pidx].m[kk][0] | A.pool[pidx].m[kk][1]) >> (8 * ii)) & 0xffu;
-                const f2x AX = bc(a.x), AY = bc(a.y), AZ = bc(a.z);
-                float r2min = 0.f;
-#pragma unroll
-                for (int h = 0; h < 2; h++) {
-                    const ulonglong2 X = *reinterpret_cast<const ulonglong2*>(xs + 4 * h);
-                    const ulonglong2 Y = *reinterpret_cast<const ulonglong2*>(ys + 4 * h);
-                    const ulonglong2 Z = *reinterpret_cast<const ulonglong2*>(zs + 4 * h);
-                    const f2x DX0 = sub2(X.x, AX), DY0 = sub2(Y.x, AY), DZ0 = sub2(Z.x, AZ);
-                    const f2x DX1 = sub2(X.y, AX), DY1 = sub2(Y.y, AY), DZ1 = sub2(Z.y, AZ);
-                    const float2 R0 = upk(fma2(DZ0, DZ0, fma2(DY0, DY0, mul2(DX0, DX0))));
-                    const float2 R1 = upk(fma2(DZ1, DZ1, fma2(DY1, DY1, mul2(DX1, DX1))));
-                    const unsigned rb = row >> (4 * h);
-                    const float inf = __int_as_float(0x7f800000);
-                    const float m4 = fminf(fminf((rb & 1u) ? R0.x : inf, (rb & 2u) ? R0.y : inf),
-                                           fminf((rb & 4u) ? R1.x : inf, (rb & 8u) ? R1.y : inf));
-                    r2min = h ? fminf(r2min, m4) : m4;
-                }
-                hit = r2min < A.rli2;
-            }
-            const unsigned bits = __ballot_sync(full, hit && m < total);
-            if (lane == 0) s_pass[wib][base >> 3] = bits;
-        }
-        __syncwarp();
-        // each entry collects its items' hits (items o .. o + pc - 1, in imask bit order)
-        unsigned my_nm = 0u;
-        {
-            unsigned mm = imask;
-            for (int m = incl - pc; mm; m++) {
-                if ((s_pass[wib][m >> 3] >> (4 * (m & 7))) & 0xfu) my_nm |= mm & (0u - mm);
-                mm &= mm - 1u;
-            }
-        }
+        const unsigned my_nm = prune_chunk_packed(A, S, lane, c0, se.cj_end, my);
         const unsigned keep = __ballot_sync(full, my_nm != 0u);
         if (my_nm) {
             nbx_cj_entry o;
@@ -792,6 +812,62 @@ __global__ void __launch_bounds__(PRUNE_THREADS, NBX_PRUNE_MINB) k_prune_packed(
         }
         kept += __popc(keep);
         __syncwarp();
+    }
+    if (lane == 0) {
+        nbx_sci_entry o = se;
+        o.cj_end = se.cj_start + kept;
+        A.sci_in[e] = o;
+    }
+}
+
+// Split prune for short lists (fewer sci entries than the machine holds warps: small boxes, DD
+// halo lists): one warp per (entry, 32-entry chunk) instead of per entry, kept entries
+// compacted at the chunk's own offset in a scratch copy, then k_prune_gather moves each entry's
+// chunks together -- the same inner list as k_prune_packed, with up to `chunks` x the warps
+__global__ void __launch_bounds__(PRUNE_THREADS, NBX_PRUNE_MINB) k_prune_split(PruneArgs A, int chunks,
+                                                                                nbx_cj_entry* tmp, int* kept_n)
+{
+    constexpr int W = PRUNE_THREADS / 32;
+    __shared__ __align__(16) PruneWarpSmem s_w[W];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int we = w / chunks, c = w - we * chunks;
+    const int e = A.part + A.nparts * we;
+    if (e >= A.n_sci) return;
+    const unsigned full = 0xffffffffu, lt = (1u << lane) - 1u;
+    PruneWarpSmem& S = s_w[wib];
+    const nbx_sci_entry se = A.sci[e];
+    const int c0 = se.cj_start + 32 * c;
+    if (c0 >= se.cj_end) {
+        if (lane == 0) kept_n[w] = 0;
+        return;
+    }
+    prune_stage_i(A, se, S, lane);
+    nbx_cj_entry my;
+    const unsigned my_nm = prune_chunk_packed(A, S, lane, c0, se.cj_end, my);
+    const unsigned keep = __ballot_sync(full, my_nm != 0u);
+    if (my_nm) {
+        nbx_cj_entry o;
+        o.cj = my.cj;
+        o.meta = my_nm | (my.meta & ~0xffu);
+        tmp[c0 + __popc(keep & lt)] = o;
+    }
+    if (lane == 0) kept_n[w] = __popc(keep);
+}
+
+__global__ void __launch_bounds__(256) k_prune_gather(PruneArgs A, int chunks, const nbx_cj_entry* __restrict__ tmp,
+                                                      const int* __restrict__ kept_n)
+{
+    const int lane = threadIdx.x & 31;
+    const int we = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int e = A.part + A.nparts * we;
+    if (e >= A.n_sci) return;
+    const nbx_sci_entry se = A.sci[e];
+    int kept = 0;
+    for (int c = 0; c < chunks; c++) {
+        const int n = kept_n[we * chunks + c];
+        if (lane < n) A.cj_in[se.cj_start + kept + lane] = tmp[se.cj_start + 32 * c + lane];
+        kept += n;
     }
     if (lane == 0) {
         nbx_sci_entry o = se;
@@ -1017,6 +1093,17 @@ static void sort_entries(nbx_ctx* ctx, List& L, cudaStream_t st)
     ctx->launches += 4;
 }
 
+// split prune when the entries to prune fill less than half a wave of prune warps (16 of the
+// 32 per SM): there the per-entry warps are latency-bound and the chunks give the SMs more
+// warps (water 3k 24.6 -> 19.8 us, RNase 24k 53.4 -> 47.7 us); from about a wave on, the
+// chunks' repeated i staging and the gather pass cost more (82k membrane 70 -> 88 us, STMV
+// 0.58 -> 0.89 ms forced on; profiles/r02_prune_split.jsonl)
+static bool prune_split_on(const nbx_ctx* ctx, int nw)
+{
+    if (ctx->prune_split >= 0) return ctx->prune_split > 0;
+    return nw < 16 * ctx->num_sms;
+}
+
 void prune(nbx_ctx* ctx, int l, int part, int nparts, cudaStream_t st)
 {
     List& L = ctx->list[l];
@@ -1028,7 +1115,13 @@ void prune(nbx_ctx* ctx, int l, int part, int nparts, cudaStream_t st)
     const int nw = (int)((L.n_sci - part + nparts - 1) / nparts);
     if (nw <= 0) return;
     const int blocks = (nw * 32 + PRUNE_THREADS - 1) / PRUNE_THREADS;
-    if (ctx->prune_kernel == 0) k_prune<<<blocks, PRUNE_THREADS, 0, st>>>(A);
+    if (ctx->prune_kernel == 2 && L.prune_chunks >= 2 && prune_split_on(ctx, nw)) {
+        const int chunks = L.prune_chunks;
+        k_prune_split<<<(int)(((long long)nw * chunks * 32 + PRUNE_THREADS - 1) / PRUNE_THREADS), PRUNE_THREADS, 0, st>>>(
+            A, chunks, L.prune_tmp.p, L.prune_kept.p);
+        k_prune_gather<<<(nw * 32 + 255) / 256, 256, 0, st>>>(A, chunks, L.prune_tmp.p, L.prune_kept.p);
+        ctx->launches += 2;
+    } else if (ctx->prune_kernel == 0) k_prune<<<blocks, PRUNE_THREADS, 0, st>>>(A);
     else if (ctx->prune_kernel == 1) k_prune_lanes<<<blocks, PRUNE_THREADS, 0, st>>>(A);
     else if (ctx->prune_kernel == 3) k_prune_fixed<<<blocks, PRUNE_THREADS, 0, st>>>(A);
     else k_prune_packed<<<blocks, PRUNE_THREADS, 0, st>>>(A); // default
@@ -1185,6 +1278,17 @@ static void search_end(nbx_ctx* ctx, int l, cudaStream_t st, SearchStage& S)
         L.tsci.ensure((size_t)NBX_NSHIFT * nsci);
         L.tcj.ensure((size_t)L.cap_cj * nsci);
         L.tpool.ensure((size_t)L.cap_pool * nsci);
+    }
+    // split-prune scratch (sized here, never inside a step): chunks of the longest sci's
+    // entries; an entry is at most one sci's cj entries (fl[1] is the largest of those)
+    L.prune_chunks = 0;
+    if (ctx->prune_kernel == 2 && L.n_sci > 0 && prune_split_on(ctx, (int)L.n_sci)) {
+        const int chunks = (fl[1] + 31) / 32;
+        if (chunks >= 2) {
+            L.prune_tmp.ensure(L.n_cj + 1);
+            L.prune_kept.ensure((size_t)L.n_sci * chunks);
+            L.prune_chunks = chunks;
+        }
     }
     L.built = true;
     prune(ctx, l, 0, 1, st);

@@ -110,13 +110,17 @@ def test_prune_after_motion(gpu, name):
 @pytest.mark.parametrize("name", ["rnase24k", "water3k"])
 def test_prune_kernels_identical(gpu, name, monkeypatch):
     """All prune kernels (NBX_PRUNE_KERNEL=0: lane per cj entry, 1: lane per i atom, 2: packed
-    active tiles) give the oracle's inner list bit-exactly after motion, whole and rolling."""
+    active tiles, per entry and -- NBX_PRUNE_SPLIT=1 -- split into 32-entry chunks plus a
+    gather, the short-list form) give the oracle's inner list bit-exactly after motion, whole
+    and rolling."""
     s = get_system(name)
     rng = np.random.default_rng(11)
     x1 = (s.x + rng.uniform(-0.04, 0.04, size=s.x.shape)).astype(np.float32)
     lists = []
-    for kern in ("0", "1", "2"):
+    variants = (("0", "0"), ("1", "0"), ("2", "0"), ("2", "1"))
+    for kern, split in variants:
         monkeypatch.setenv("NBX_PRUNE_KERNEL", kern)
+        monkeypatch.setenv("NBX_PRUNE_SPLIT", split)
         nb, on, xd = run_pair(s)
         nb.put_x(to_dev(x1))
         for p in range(2):
@@ -124,8 +128,8 @@ def test_prune_kernels_identical(gpu, name, monkeypatch):
         lists.append(nb.pairlist(1))
     on.put_x(x1)
     on.prune()
-    for kern, lg in zip("012", lists):
-        assert_lists_equal(lg, on.list.export(1), f"{name} prune kernel {kern}")
+    for (kern, split), lg in zip(variants, lists):
+        assert_lists_equal(lg, on.list.export(1), f"{name} prune kernel {kern} split {split}")
 
 
 def test_rolling_prune_parts(gpu):
