@@ -5,19 +5,23 @@
 // grid columns 32 at a time (one binary search over the column's z-sorted slabs per lane,
 // all in flight together; columns whose x-y box is out of range are dropped by an exact
 // pre-test), prefix-sums their j-cluster counts and tests the candidates in two phases: one
-// candidate per lane against the super-cluster bounding box, then the survivors' 8
-// i-cluster tiles spread over the lanes (lane = survivor * 8 + i-cluster), all at
-// rlist_outer.  Exclusion masks are only computed for tiles that contain an excluded
-// partner (each i-atom's partners are mapped to their j-cluster through the grid's
-// gid -> slot map into a per-warp shared-memory list), contain filler slots, lie on the
-// diagonal (the nonlocal list has no diagonal: every home x halo pair is computed there).  The list is written
-// deterministically at ballot/popc ranks -- the canonical (sci, shift, cj) order of the CPU
-// oracle (ora_search), bit for bit: in one pass into per-sci private regions (capacity
-// learned from the previous search) plus a compaction, or, for the first search and on
-// overflow, a count pass, exclusive scans and a fill pass.
+// candidate per lane against the super-cluster bounding box (survivors and their boxes go to
+// a per-warp shared-memory table), then the survivors' 8 i-cluster tiles spread over the
+// lanes (lane = survivor * 8 + i-cluster), all at rlist_outer.  Explicit masks are computed
+// only for tiles that contain an excluded partner (each i-atom's partners are mapped to their
+// j-cluster through the grid's gid -> slot map into a per-warp shared-memory list, behind an
+// exact 64-bit filter), contain filler slots or lie on the diagonal (the nonlocal list has no
+// diagonal: every home x halo pair is computed there) -- by the whole warp, one tile per pass,
+// one atom pair per lane.  The list is written deterministically at ballot/popc ranks -- the
+// canonical (sci, shift, cj) order of the CPU oracle (ora_search), bit for bit: in one pass
+// into per-sci private regions (capacity learned from the previous search) plus a
+// compaction, or, for the first search and on overflow, a count pass, exclusive scans and a
+// fill pass.
 //
-// Prune: one warp per sci entry, one cj entry per lane; every active tile tests its atom
-// pairs at rlist_inner and stops at the first hit; kept entries are compacted in order.
+// Prune (default k_prune_packed): one warp per sci entry; per 32-entry chunk the active tiles
+// are compacted into an item table and tested 8 per warp pass (4 lanes per tile, packed
+// FP32x2 r^2 at rlist_inner); kept entries are compacted in order.  Short lists use the split
+// form (a warp per chunk + a gather).  k_prune / k_prune_lanes / k_prune_fixed are opt-ins.
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
