@@ -96,6 +96,8 @@ def test_halo_entry_points_validate_arguments():
     assert lib.nbx_halo_pack_x(None, None, -1, None, None, None) == 1
     assert lib.nbx_halo_unpack_add_f(None, None, 5, None, None) == 1
     assert lib.nbx_halo_pack_x(None, None, 0, None, None, None) == 0
+    # the overlapped DD search step rejects a missing context before touching any stream
+    assert lib.nbx_grid_search_pair(None, 0, None, None, None, None, 0, None, None, None, None, None, None) != 0
 
 
 def test_pme_no_cpu_fallback_and_validation():
