@@ -31,6 +31,7 @@ __global__ void k_get_f(int n, const int* __restrict__ islot, const float4* __re
 {
     const int a = blockIdx.x * blockDim.x + threadIdx.x;
     if (a >= n) return;
+    NBX_DCHECK(islot[a] >= 0);
     const float4 v = fc[islot[a]];
     if (accumulate) {
         f[3 * a] += v.x;

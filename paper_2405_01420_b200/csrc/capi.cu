@@ -162,7 +162,7 @@ extern "C" {
 
 NBX_API const char* nbx_last_error(void) { return g_err.c_str(); }
 
-NBX_API const char* nbx_version(void) { return "nbx 0.1 (sm_100a)"; }
+NBX_API const char* nbx_version(void) { return NBX_CHECKED ? "nbx 0.1 (sm_100a, checked)" : "nbx 0.1 (sm_100a)"; }
 
 NBX_API int nbx_derive_consts(const nbx_params* p, nbx_consts* out)
 {

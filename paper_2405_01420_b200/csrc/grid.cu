@@ -97,6 +97,7 @@ struct SlabArgs {
     float4* wrapk;
     int* slotmap;
     int* islot;
+    int natoms_global; // slotmap extent (checked builds)
 };
 
 // rank of this lane's key among the real lanes of the same group (ties impossible: idx)
@@ -147,6 +148,7 @@ __global__ void k_slab(SlabArgs A)
     if (real) {
         int slot = slot0 + off;
         int g = A.gid_in ? A.gid_in[idx] : idx;
+        NBX_DCHECK(g >= 0 && g < A.natoms_global && slot0 + off < 32 * A.nsci);
         float q = A.q_g[g];
         A.order[slot] = idx;
         A.gid[slot] = g;
@@ -371,6 +373,7 @@ static void grid_end(nbx_ctx* ctx, int g, cudaStream_t st, const GridStage& S)
         S.wrapk = G.wrapk.p;
         S.slotmap = G.slotmap.p;
         S.islot = G.islot.p;
+        S.natoms_global = ctx->natoms_global;
         int threads = 128, blocks = (G.nsci * 32 + threads - 1) / threads;
         k_slab<<<blocks, threads, 0, st>>>(S);
         ctx->launches++;

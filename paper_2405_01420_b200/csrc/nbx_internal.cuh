@@ -27,6 +27,25 @@ struct CudaError {
     const char* what;
 };
 
+// Checked builds (-DNBX_CHECKED=1, tools/checked_build.py): every data-dependent index the
+// kernels read from lists, grids or caller arrays is range-checked on the device, and a
+// violation fails a device assert (the stand-in for compute-sanitizer memcheck,
+// which this GPU pool does not run).  Compiled out of the shipped library.
+#ifndef NBX_CHECKED
+#define NBX_CHECKED 0
+#endif
+#if NBX_CHECKED
+#undef NDEBUG
+#include <cassert>
+// device assert: the failed condition (tagged NBX_DCHECK) is printed and the kernel stops with
+// cudaErrorAssert, which every later call on the context reports
+#define NBX_DCHECK(cond) assert((cond) && "NBX_DCHECK")
+#else
+#define NBX_DCHECK(cond) \
+    do {                 \
+    } while (0)
+#endif
+
 #define NBX_CUDA(call)                                                               \
     do {                                                                             \
         cudaError_t _e = (call);                                                     \

@@ -72,6 +72,7 @@ struct SearchArgs {
     // single pass: per-sci private regions of capacity cap_cj / cap_pool, compacted afterwards
     int cap_cj, cap_pool;
     int* flags; // [0] overflow, [1] max n_cj per sci, [2] max n_pool per sci
+    int ncl_j;  // j clusters in grid j (checked builds)
 };
 
 enum { SEARCH_COUNT = 0, SEARCH_FILL = 1, SEARCH_SINGLE = 2 };
@@ -321,6 +322,7 @@ __global__ void __launch_bounds__(SEARCH_THREADS, NBX_SEARCH_MINB) k_search(Sear
                     bool pass = (t < total) && !(A.mode == NBX_LIST_LOCAL && central && cj < 4 * sci);
                     float4 blo = make_float4(0.f, 0.f, 0.f, 0.f), bhi = blo;
                     if (pass) {
+                        NBX_DCHECK(cj >= 0 && cj < A.ncl_j);
                         blo = A.bb_cj[2 * cj];
                         bhi = A.bb_cj[2 * cj + 1];
                         pass = blo.w != 0.0f && bb_dist2(slo, shi, v, blo, bhi) < A.rl2;
@@ -475,6 +477,7 @@ struct PruneArgs {
     float rli2;
     nbx_sci_entry* sci_in;
     nbx_cj_entry* cj_in;
+    int n_cj, n_pool, nsci_i, ncl_j; // list / grid extents (checked builds)
 };
 
 constexpr int PRUNE_THREADS = 256;
@@ -677,6 +680,8 @@ struct PruneWarpSmem {
 // i atoms of sci entry se (+ its shift) into the warp's staging
 __device__ __forceinline__ void prune_stage_i(const PruneArgs& A, const nbx_sci_entry& se, PruneWarpSmem& S, int lane)
 {
+    NBX_DCHECK(se.sci >= 0 && se.sci < A.nsci_i && se.shift >= 0 && se.shift < NBX_NSHIFT && se.cj_start >= 0 &&
+               se.cj_end <= A.n_cj);
     const float3 v = shift_vec(se.shift, A.box);
     const float4 t0 = A.xq_i[32 * se.sci + lane];
     S.xi[lane] = make_float4(__fadd_rn(t0.x, v.x), __fadd_rn(t0.y, v.y), __fadd_rn(t0.z, v.z), 0.f);
@@ -693,6 +698,7 @@ __device__ __forceinline__ unsigned prune_chunk_packed(const PruneArgs& A, Prune
     my.cj = 0;
     my.meta = 0u;
     if (lane < cnt) my = A.cj[c0 + lane];
+    NBX_DCHECK(lane >= cnt || (my.cj >= 0 && my.cj < A.ncl_j && (int)(my.meta >> 8) < A.n_pool));
     __syncwarp();
     for (int r = 0; r < 8 && 4 * r < cnt; r++) {
         const int t = 4 * r + (lane >> 3);
@@ -854,6 +860,7 @@ __global__ void __launch_bounds__(PRUNE_THREADS, NBX_PRUNE_MINB) k_prune_split(P
         nbx_cj_entry o;
         o.cj = my.cj;
         o.meta = my_nm | (my.meta & ~0xffu);
+        NBX_DCHECK(c0 + __popc(keep & lt) < A.n_cj);
         tmp[c0 + __popc(keep & lt)] = o;
     }
     if (lane == 0) kept_n[w] = __popc(keep);
@@ -1032,6 +1039,10 @@ static PruneArgs prune_args(nbx_ctx* ctx, List& L)
     A.rli2 = ctx->c.rli2;
     A.sci_in = L.sci_in.p;
     A.cj_in = L.cj_in.p;
+    A.n_cj = (int)L.n_cj;
+    A.n_pool = (int)L.n_pool;
+    A.nsci_i = ctx->grid[L.gi].nsci;
+    A.ncl_j = ctx->grid[L.gj].nslots / 8;
     return A;
 }
 
@@ -1184,6 +1195,7 @@ static void search_begin(nbx_ctx* ctx, int l, cudaStream_t st, SearchStage& S)
     A.rl = ctx->p.rlist_outer;
     A.rl2 = ctx->c.rlo2;
     A.rlm = ctx->p.rlist_outer * 1.001f + 1.0e-4f;
+    A.ncl_j = GJ.nslots / 8;
 
     const int n3 = 3 * (nsci + 1);
     L.counts.ensure(n3);
