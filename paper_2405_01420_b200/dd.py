@@ -441,29 +441,34 @@ class DomainDecomposition:
         lo_l = np.array([lo[d] if self.dims[d] > 1 else 0.0 for d in range(3)], np.float32)
         size_n = np.array([self.D[d] + 2 * self.rl if self.dims[d] > 1 else self.box[d] for d in range(3)], np.float32)
         lo_n = np.array([lo[d] - self.rl if self.dims[d] > 1 else 0.0 for d in range(3)], np.float32)
-        eng = self.engine
         self._tick("buffers")
-        if hasattr(eng, "grid_search_pair") and os.environ.get("NBX_DD_PAIR_SEARCH", "1") != "0":
-            # home grid + local list on this stream, halo grid + nonlocal list on the side
-            # stream, overlapped (nbx_grid_search_pair)
-            if self._side is None:
-                self._side = torch.cuda.Stream(device=self.device)
-            eng.grid_search_pair(self.x_ext[:self.n_home], self.gid_ext[:self.n_home], lo_l, size_l,
-                                 self.x_ext[self.n_home:], self.gid_ext[self.n_home:], lo_n, size_n, self._side)
-            self._tick("grids_searches")
-        else:
-            eng.grid_build(0, self.x_ext[:self.n_home], self.gid_ext[:self.n_home], lo_l, size_l)
-            self._tick("grid0")
-            eng.search(0)
-            self._tick("search0")
-            eng.grid_build(1, self.x_ext[self.n_home:], self.gid_ext[self.n_home:], lo_n, size_n)
-            self._tick("grid1")
-            eng.search(1)
-            self._tick("search1")
+        self._grids_and_searches(size_l, lo_l, size_n, lo_n)
         if self.halo == "p2p":
             self._peer_map()
             self._tick("peer_map")
         return self.n_home
+
+    def _grids_and_searches(self, size_l, lo_l, size_n, lo_n):
+        """Home grid + local list and halo grid + nonlocal list of a search step.  On the GPU
+        engine both halves run overlapped, the halo half on the side stream
+        (nbx_grid_search_pair; NBX_DD_PAIR_SEARCH=0 restores the four sequential calls)."""
+        eng = self.engine
+        xh, gh = self.x_ext[:self.n_home], self.gid_ext[:self.n_home]
+        xn, gn = self.x_ext[self.n_home:], self.gid_ext[self.n_home:]
+        if hasattr(eng, "grid_search_pair") and os.environ.get("NBX_DD_PAIR_SEARCH", "1") != "0":
+            if self._side is None:
+                self._side = self.torch.cuda.Stream(device=self.device)
+            eng.grid_search_pair(xh, gh, lo_l, size_l, xn, gn, lo_n, size_n, self._side)
+            self._tick("grids_searches")
+        else:
+            eng.grid_build(0, xh, gh, lo_l, size_l)
+            self._tick("grid0")
+            eng.search(0)
+            self._tick("search0")
+            eng.grid_build(1, xn, gn, lo_n, size_n)
+            self._tick("grid1")
+            eng.search(1)
+            self._tick("search1")
 
     def dd_geom(self):
         """nbx_dd_geom of this rank: domain, neighbour ranks, half-shell import offsets."""
@@ -553,24 +558,7 @@ class DomainDecomposition:
         self.f_ext.zero_()
         self.pulses = []  # the message-passing halo plan is not built on this path
         size_l, lo_l, size_n, lo_n = self._grid_boxes()
-        eng = self.engine
-        if hasattr(eng, "grid_search_pair") and os.environ.get("NBX_DD_PAIR_SEARCH", "1") != "0":
-            # home grid + local list on this stream, halo grid + nonlocal list on the side
-            # stream, overlapped (nbx_grid_search_pair)
-            if self._side is None:
-                self._side = torch.cuda.Stream(device=self.device)
-            eng.grid_search_pair(self.x_ext[:self.n_home], self.gid_ext[:self.n_home], lo_l, size_l,
-                                 self.x_ext[self.n_home:], self.gid_ext[self.n_home:], lo_n, size_n, self._side)
-            self._tick("grids_searches")
-        else:
-            eng.grid_build(0, self.x_ext[:self.n_home], self.gid_ext[:self.n_home], lo_l, size_l)
-            self._tick("grid0")
-            eng.search(0)
-            self._tick("search0")
-            eng.grid_build(1, self.x_ext[self.n_home:], self.gid_ext[self.n_home:], lo_n, size_n)
-            self._tick("grid1")
-            eng.search(1)
-            self._tick("search1")
+        self._grids_and_searches(size_l, lo_l, size_n, lo_n)
         self._peer_owner = B["owner"][:nhalo]
         self._peer_home = B["home"][:nhalo]
         self._peer_shift = B["shift"][:nhalo]
