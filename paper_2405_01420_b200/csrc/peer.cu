@@ -123,12 +123,13 @@ __global__ void k_peer_wait(const unsigned* flags, int world, int kind, unsigned
 // grid-0 X buffer op that also publishes the home coordinates
 __global__ void k_peer_put_x(int nslots, const int* __restrict__ order, const float4* __restrict__ wrapk,
                              const float* __restrict__ x, float3 box, float4* __restrict__ xq,
-                             float4* __restrict__ xpub)
+                             float4* __restrict__ xpub, int cap)
 {
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= nslots) return;
     const int a = order[s];
     if (a < 0) return;
+    NBX_DCHECK(a < cap);
     const float4 k = wrapk[s];
     const float x0 = x[3 * a], x1 = x[3 * a + 1], x2 = x[3 * a + 2];
     xq[s] = make_float4(__fmaf_rn(-k.x, box.x, x0), __fmaf_rn(-k.y, box.y, x1), __fmaf_rn(-k.z, box.z, x2), k.w);
@@ -157,6 +158,7 @@ __global__ void k_peer_get_f(int n, const int* __restrict__ islot, const float4*
 {
     const int a = blockIdx.x * blockDim.x + threadIdx.x;
     if (a >= n) return;
+    NBX_DCHECK(islot[a] >= 0);
     const float4 v = fc[islot[a]];
     const float4 r = __ldcg(inbox + a);
     inbox[a] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -350,7 +352,7 @@ void peer_put_x(nbx_ctx* ctx, const float* x, unsigned seq, cudaStream_t st)
     if (G.nslots > 0) {
         k_peer_put_x<<<(G.nslots + 255) / 256, 256, 0, st>>>(G.nslots, G.order.p, G.wrapk.p, x,
                                                              make_float3(ctx->box[0], ctx->box[1], ctx->box[2]),
-                                                             G.xq.p, P.xpub);
+                                                             G.xq.p, P.xpub, P.cap);
         ctx->launches++;
         NBX_CUDA(cudaGetLastError());
     }
@@ -450,6 +452,7 @@ __global__ void k_rp_pull_home(nbx_dd_geom G, const float4* const* __restrict__ 
 {
     const int r = G.src_rank[blockIdx.y];
     const int n = __ldcg(cnt[r]);
+    NBX_DCHECK(r >= 0 && n >= 0 && n <= cap); // every rank publishes at most the common capacity
     for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < n; a += gridDim.x * blockDim.x) {
         const float4 p = __ldcg(xpub[r] + a);
         const float w0 = rp_wrap(p.x, G.box[0]), w1 = rp_wrap(p.y, G.box[1]), w2 = rp_wrap(p.z, G.box[2]);
@@ -492,6 +495,7 @@ __global__ void k_rp_pull_halo(nbx_dd_geom G, const float4* const* __restrict__ 
     const int oi = blockIdx.y;
     const int r = G.off_rank[oi];
     const int n = __ldcg(cnt[r] + 1);
+    NBX_DCHECK(r >= 0 && n >= 0 && n < (1 << 26)); // the home index fits the 26-bit key field
     for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < n; a += gridDim.x * blockDim.x) {
         const float4 p = __ldcg(xpub2[r] + a);
         const float x[3] = {__fadd_rn(p.x, G.off_shift[oi][0]), __fadd_rn(p.y, G.off_shift[oi][1]),
