@@ -664,7 +664,10 @@ __global__ void __launch_bounds__(PRUNE_THREADS) k_prune_lanes(PruneArgs A)
 #define NBX_PRUNE_JS 8
 #endif
 #ifndef NBX_PRUNE_MINB
-#define NBX_PRUNE_MINB 1
+// 6 CTAs/SM (<= 40 registers, no spills; 6 x 33 KB of staging fits the SM's shared memory):
+// 12 M prune 3.78 -> 3.49 ms, STMV 0.584 -> 0.555 ms vs the unconstrained 62 registers at 4
+// (82k membrane +6 %; profiles/r02_prune_minb.jsonl)
+#define NBX_PRUNE_MINB 6
 #endif
 constexpr int PRUNE_JS = NBX_PRUNE_JS;
 
