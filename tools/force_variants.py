@@ -12,7 +12,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "scratch", "variants")
 VARIANTS = {
     "base": [],
-    "pm1": ["-DNBX_PRUNE_MINB=1"],
+    "s16": ["-DNBX_SEARCH_MINB=16"],
 }
 
 
