@@ -142,6 +142,8 @@ struct ForceConsts {
     float ewn[6], ewd[5]; // F-only Ewald: -beta^3 G as N(r2) / D(r2), D monic (pairmath.cuh)
     alignas(8) float ewnd[10]; // (ewn[k], ewd[k]) interleaved: one 64-bit constant per FFMA2
     alignas(8) float ehnd[12]; // energy kernels' H(z) rational: (num, den) coefficient pairs
+    alignas(8) float ehbd[12]; // NBX_VF_H: the same with the numerator scaled by beta (beta H)
+    float ehb0, two_sh_lj6;    // beta * H's last numerator coefficient; 2 sh_lj6
 };
 
 } // namespace nbx

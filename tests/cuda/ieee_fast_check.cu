@@ -1,4 +1,4 @@
-// Bit-exactness check of pairmath.cuh's call-free IEEE fast paths (div_rn_fast, sqrt_rn_fast)
+// Bit-exactness check of pairmath.cuh's call-free IEEE fast paths (div_rn_fast, rcp_rn_fast, sqrt_rn_fast)
 // against the compiler's __fdiv_rn / __fsqrt_rn over random operands in the energy kernels'
 // domain: r2 in [1e-6, 1e12] (sqrt and 1/sqrt), numerators |n| in [1e-30, 1e30] of either sign
 // over divisors in [1, 1e12] (the fitted Ewald rationals' denominators are >= 1).
@@ -30,7 +30,7 @@ __global__ void k_check(uint64_t n, uint32_t seed, unsigned long long* bad)
         float a = loguni(hash(h2), -99.6f, 99.6f);             // 1e-30 .. 1e30
         if (h1 & 1u) a = -a;
         const float s1 = nbx::sqrt_rn_fast(r2), s2 = __fsqrt_rn(r2);
-        const float i1 = nbx::div_rn_fast(1.0f, s1), i2 = __fdiv_rn(1.0f, s2);
+        const float i1 = nbx::rcp_rn_fast(s1), i2 = __fdiv_rn(1.0f, s2);
         const float d1 = nbx::div_rn_fast(a, b), d2 = __fdiv_rn(a, b);
         nb += (__float_as_uint(s1) != __float_as_uint(s2)) + (__float_as_uint(i1) != __float_as_uint(i2)) +
               (__float_as_uint(d1) != __float_as_uint(d2));

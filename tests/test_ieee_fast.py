@@ -1,6 +1,7 @@
-"""The energy kernels' call-free IEEE division / square root (pairmath.cuh div_rn_fast,
-sqrt_rn_fast) are bit-identical to __fdiv_rn / __fsqrt_rn over the kernels' operand domain --
-the premise of bit-identical per-pair energies with the oracle."""
+"""The energy kernels' call-free IEEE division / reciprocal / square root (pairmath.cuh
+div_rn_fast, rcp_rn_fast, sqrt_rn_fast) are bit-identical to __fdiv_rn / __fsqrt_rn over the
+kernels' operand domain -- the premise of bit-identical per-pair energies with the oracle
+(DESIGN.md section 5)."""
 import os
 import subprocess
 

@@ -16,8 +16,8 @@ sources and derivations):
     E = f sum_inter q q / r - f k_rf |mu_total|^2 (Onsager cavity energy of the dipole).
 
 Tolerances.  float64 tools (oracle/brute.py real space, oracle/pme.py direct and PME
-reciprocal sums): 1e-7.  The fp32 kernels (C oracle and libnbx, bit-identical in the energy
-kernels): 1e-6, the north_star energy bar, for the Madelung energies too (measured 2.6e-7
+reciprocal sums): 1e-7.  The fp32 kernels (C oracle and libnbx, per-pair Coulomb energies
+bit-identical in the energy kernels): 1e-6, the north_star energy bar, for the Madelung energies too (measured 2.6e-7
 NaCl, 5.3e-7 CsCl with the (6,5) H rational of the energy path; round 1's (5,4) fit, 5e-7
 relative error amplified ~3x by the 1/r - erf(beta r)/r cancellation at the nearest-neighbour
 distance, gave 1.7e-6) and for LJ and reaction field.  Forces of the perfect crystals vanish

@@ -12,25 +12,34 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "scratch", "variants")
 VARIANTS = {
     "base": [],
-    "s16": ["-DNBX_SEARCH_MINB=16"],
+    "vf0": ["-DNBX_VF_RINV=0", "-DNBX_VF_G=0", "-DNBX_VF_H=0", "-DNBX_VF_LJ12=0"],  # IEEE-exact energy kernels
+    "e3": ["-DNBX_FORCE_MINB_ENERGY=3"],  # energy kernels at 3 CTAs/SM (<= 85 registers)
 }
+# sources whose objects depend on the -D flags (the rest are built once and shared)
+FLAG_SOURCES = ("force.cu",)
 
 
 def build():
     sys.path.insert(0, ROOT)
     from paper_2405_01420_b200 import build as B
     os.makedirs(OUT, exist_ok=True)
+    shared = {}
     for name, flags in VARIANTS.items():
         objs = []
         for src in B.SOURCES:
+            if src not in FLAG_SOURCES and src in shared:
+                objs.append(shared[src])
+                continue
             o = os.path.join(OUT, f"{name}_{src}.o")
             extra = B.PER_FILE.get(src, [])
             cmd = [B._nvcc(), *B.ARCH, *B.NVCC_FLAGS, *extra, *flags, "-c", os.path.join(B.CSRC, src), "-o", o]
             subprocess.check_call(cmd, stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
             objs.append(o)
+            if src not in FLAG_SOURCES:
+                shared[src] = o
         subprocess.check_call([B._nvcc(), *B.ARCH, "-shared", "-o", os.path.join(OUT, f"libnbx_{name}.so"), *objs,
                                "-lcudart", "-lcufft"])
-        print("built", name)
+        print("built", name, flush=True)
 
 
 def run_one(name, cfg, reps=20):
