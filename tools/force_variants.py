@@ -12,8 +12,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "scratch", "variants")
 VARIANTS = {
     "base": [],
-    "vf0": ["-DNBX_VF_RINV=0", "-DNBX_VF_G=0", "-DNBX_VF_H=0", "-DNBX_VF_LJ12=0"],  # IEEE-exact energy kernels
-    "e3": ["-DNBX_FORCE_MINB_ENERGY=3"],  # energy kernels at 3 CTAs/SM (<= 85 registers)
+    "tpe": ["-DNBX_TILE_PAIRS_E=1"],  # energy kernels: active tile pairs in one basic block
+    "tpe_u2": ["-DNBX_TILE_PAIRS_E=1", "-DNBX_FORCE_MINB_ENERGY=1"],  # ... at 1 CTA/SM bound (all registers)
 }
 # sources whose objects depend on the -D flags (the rest are built once and shared)
 FLAG_SOURCES = ("force.cu",)
