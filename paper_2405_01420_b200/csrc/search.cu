@@ -671,6 +671,14 @@ __global__ void __launch_bounds__(PRUNE_THREADS) k_prune_lanes(PruneArgs A)
 #endif
 constexpr int PRUNE_JS = NBX_PRUNE_JS;
 
+#ifndef NBX_PRUNE_REP
+// 1: a first sweep tests one row of every active tile (i atom 1 against the 8 j atoms, one lane
+// per tile, 32 tiles per warp instruction); only the tiles it does not keep get the full 32-pair
+// test.  The row's r^2 are the full test's own (same packed operations), so the kept set and the
+// lists are unchanged
+#define NBX_PRUNE_REP 1
+#endif
+
 // per-warp shared staging of the packed prune
 struct PruneWarpSmem {
     float xj[3][32][PRUNE_JS];
@@ -678,7 +686,64 @@ struct PruneWarpSmem {
     unsigned pass[32]; // per pass: the hit ballot (4 lanes per item)
     unsigned pidx[32];
     unsigned char item[256]; // entry << 3 | i-cluster
+#if NBX_PRUNE_REP
+    unsigned char hit[256];   // per item: kept
+    unsigned char item2[256]; // items the row sweep left open (indices into item)
+#endif
 };
+
+// min r^2 of i atom a against the 8 j atoms of staged row (xs, ys, zs); MASKED: pairs whose bit
+// in `row` is clear count as +inf
+template <bool MASKED>
+__device__ __forceinline__ float prune_r2min8(const float4& a, const float* xs, const float* ys, const float* zs,
+                                              unsigned row)
+{
+    const f2x AX = bc(a.x), AY = bc(a.y), AZ = bc(a.z);
+    float r2min = 0.f;
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+        const ulonglong2 X = *reinterpret_cast<const ulonglong2*>(xs + 4 * h);
+        const ulonglong2 Y = *reinterpret_cast<const ulonglong2*>(ys + 4 * h);
+        const ulonglong2 Z = *reinterpret_cast<const ulonglong2*>(zs + 4 * h);
+        const f2x DX0 = sub2(X.x, AX), DY0 = sub2(Y.x, AY), DZ0 = sub2(Z.x, AZ);
+        const f2x DX1 = sub2(X.y, AX), DY1 = sub2(Y.y, AY), DZ1 = sub2(Z.y, AZ);
+        const float2 R0 = upk(fma2(DZ0, DZ0, fma2(DY0, DY0, mul2(DX0, DX0))));
+        const float2 R1 = upk(fma2(DZ1, DZ1, fma2(DY1, DY1, mul2(DX1, DX1))));
+        float m4;
+        if (MASKED) {
+            const unsigned rb = row >> (4 * h);
+            const float inf = __int_as_float(0x7f800000);
+            m4 = fminf(fminf((rb & 1u) ? R0.x : inf, (rb & 2u) ? R0.y : inf),
+                       fminf((rb & 4u) ? R1.x : inf, (rb & 8u) ? R1.y : inf));
+        } else {
+            m4 = fminf(fminf(R0.x, R0.y), fminf(R1.x, R1.y));
+        }
+        r2min = h ? fminf(r2min, m4) : m4;
+    }
+    return r2min;
+}
+
+// one 4-lane-per-tile pass over items it (lane group g = lane / 4, row ii = lane % 4): hit of
+// this lane's row
+__device__ __forceinline__ bool prune_tile_rows(const PruneArgs& A, const PruneWarpSmem& S, unsigned it, int ii)
+{
+    const int t = it >> 3, kk = it & 7;
+    const float4 a = S.xi[4 * kk + ii];
+    const unsigned pidx = S.pidx[t];
+    const float* xs = S.xj[0][t];
+    const float* ys = S.xj[1][t];
+    const float* zs = S.xj[2][t];
+    float r2min;
+    if (!__any_sync(0xffffffffu, pidx != 0u)) {
+        r2min = prune_r2min8<false>(a, xs, ys, zs, 0xffu);
+    } else {
+        // a pass holding an excluded (pool) tile: masked pairs' r^2 replaced by +inf
+        unsigned row = 0xffu;
+        if (pidx) row = ((A.pool[pidx].m[kk][0] | A.pool[pidx].m[kk][1]) >> (8 * ii)) & 0xffu;
+        r2min = prune_r2min8<true>(a, xs, ys, zs, row);
+    }
+    return r2min < A.rli2;
+}
 
 // i atoms of sci entry se (+ its shift) into the warp's staging
 __device__ __forceinline__ void prune_stage_i(const PruneArgs& A, const nbx_sci_entry& se, PruneWarpSmem& S, int lane)
@@ -734,62 +799,50 @@ __device__ __forceinline__ unsigned prune_chunk_packed(const PruneArgs& A, Prune
     }
     S.pidx[lane] = my.meta >> 8;
     __syncwarp();
+    unsigned my_nm = 0u;
+#if NBX_PRUNE_REP
+    // sweep 1: one lane per item, row ii = 1 of its tile; the items it does not keep are
+    // compacted into item2
+    int total2 = 0;
+    for (int base = 0; base < total; base += 32) {
+        const int m = base + lane;
+        const unsigned it = m < total ? S.item[m] : 0u;
+        const bool h1 = prune_tile_rows(A, S, it, 1); // every lane: the test holds a warp vote
+        const bool hit = m < total && h1;
+        if (m < total) S.hit[m] = hit ? 1 : 0;
+        const unsigned open = __ballot_sync(full, m < total && !hit);
+        if (m < total && !hit) S.item2[total2 + __popc(open & ((1u << lane) - 1u))] = (unsigned char)m;
+        total2 += __popc(open);
+    }
+    __syncwarp();
+    // sweep 2: the full 4-row test of the open items, 8 per pass
+    for (int base = 0; base < total2; base += 8) {
+        const int m2 = base + g;
+        const unsigned mi = m2 < total2 ? S.item2[m2] : 0u;
+        const unsigned it = S.item[mi];
+        const bool hit = prune_tile_rows(A, S, it, ii);
+        const unsigned bits = __ballot_sync(full, hit && m2 < total2);
+        if (ii == 0 && m2 < total2 && ((bits >> (4 * g)) & 0xfu)) S.hit[mi] = 1;
+    }
+    __syncwarp();
+    // each entry collects its items' hits (items o .. o + pc - 1, in imask bit order)
+    {
+        unsigned mm = imask;
+        for (int m = incl - pc; mm; m++) {
+            if (S.hit[m]) my_nm |= mm & (0u - mm);
+            mm &= mm - 1u;
+        }
+    }
+#else
     for (int base = 0; base < total; base += 8) {
         const int m = base + g;
         const unsigned it = m < total ? S.item[m] : 0u;
-        const int t = it >> 3, kk = it & 7;
-        const float4 a = S.xi[4 * kk + ii];
-        const unsigned pidx = S.pidx[t];
-        const float* xs = S.xj[0][t];
-        const float* ys = S.xj[1][t];
-        const float* zs = S.xj[2][t];
-        bool hit = false;
-        if (!__any_sync(full, pidx != 0u)) {
-            const f2x AX = bc(a.x), AY = bc(a.y), AZ = bc(a.z);
-            float r2min = 0.f;
-#pragma unroll
-            for (int h = 0; h < 2; h++) {
-                const ulonglong2 X = *reinterpret_cast<const ulonglong2*>(xs + 4 * h);
-                const ulonglong2 Y = *reinterpret_cast<const ulonglong2*>(ys + 4 * h);
-                const ulonglong2 Z = *reinterpret_cast<const ulonglong2*>(zs + 4 * h);
-                const f2x DX0 = sub2(X.x, AX), DY0 = sub2(Y.x, AY), DZ0 = sub2(Z.x, AZ);
-                const f2x DX1 = sub2(X.y, AX), DY1 = sub2(Y.y, AY), DZ1 = sub2(Z.y, AZ);
-                const float2 R0 = upk(fma2(DZ0, DZ0, fma2(DY0, DY0, mul2(DX0, DX0))));
-                const float2 R1 = upk(fma2(DZ1, DZ1, fma2(DY1, DY1, mul2(DX1, DX1))));
-                const float m4 = fminf(fminf(R0.x, R0.y), fminf(R1.x, R1.y));
-                r2min = h ? fminf(r2min, m4) : m4;
-            }
-            hit = r2min < A.rli2;
-        } else {
-            // a pass holding an excluded (pool) tile: the same packed r^2, with masked
-            // pairs' r^2 replaced by +inf before the minimum
-            unsigned row = 0xffu;
-            if (pidx) row = ((A.pool[pidx].m[kk][0] | A.pool[pidx].m[kk][1]) >> (8 * ii)) & 0xffu;
-            const f2x AX = bc(a.x), AY = bc(a.y), AZ = bc(a.z);
-            float r2min = 0.f;
-#pragma unroll
-            for (int h = 0; h < 2; h++) {
-                const ulonglong2 X = *reinterpret_cast<const ulonglong2*>(xs + 4 * h);
-                const ulonglong2 Y = *reinterpret_cast<const ulonglong2*>(ys + 4 * h);
-                const ulonglong2 Z = *reinterpret_cast<const ulonglong2*>(zs + 4 * h);
-                const f2x DX0 = sub2(X.x, AX), DY0 = sub2(Y.x, AY), DZ0 = sub2(Z.x, AZ);
-                const f2x DX1 = sub2(X.y, AX), DY1 = sub2(Y.y, AY), DZ1 = sub2(Z.y, AZ);
-                const float2 R0 = upk(fma2(DZ0, DZ0, fma2(DY0, DY0, mul2(DX0, DX0))));
-                const float2 R1 = upk(fma2(DZ1, DZ1, fma2(DY1, DY1, mul2(DX1, DX1))));
-                const unsigned rb = row >> (4 * h);
-                const float inf = __int_as_float(0x7f800000);
-                const float m4 = fminf(fminf((rb & 1u) ? R0.x : inf, (rb & 2u) ? R0.y : inf),
-                                       fminf((rb & 4u) ? R1.x : inf, (rb & 8u) ? R1.y : inf));
-                r2min = h ? fminf(r2min, m4) : m4;
-            }
-            hit = r2min < A.rli2;
-        }
+        const bool hit = prune_tile_rows(A, S, it, ii);
         const unsigned bits = __ballot_sync(full, hit && m < total);
         if (lane == 0) S.pass[base >> 3] = bits;
     }
     __syncwarp();
     // each entry collects its items' hits (items o .. o + pc - 1, in imask bit order)
-    unsigned my_nm = 0u;
     {
         unsigned mm = imask;
         for (int m = incl - pc; mm; m++) {
@@ -797,6 +850,7 @@ __device__ __forceinline__ unsigned prune_chunk_packed(const PruneArgs& A, Prune
             mm &= mm - 1u;
         }
     }
+#endif
     return lane < cnt ? my_nm : 0u;
 }
 

@@ -12,11 +12,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "scratch", "variants")
 VARIANTS = {
     "base": [],
-    "tpe": ["-DNBX_TILE_PAIRS_E=1"],  # energy kernels: active tile pairs in one basic block
-    "tpe_u2": ["-DNBX_TILE_PAIRS_E=1", "-DNBX_FORCE_MINB_ENERGY=1"],  # ... at 1 CTA/SM bound (all registers)
+    "rep0": ["-DNBX_PRUNE_REP=0"],  # prune: every active tile gets the full 32-pair test
+    "rep1m5": ["-DNBX_PRUNE_MINB=5"],  # row sweep at 5 CTAs/SM (no spills)
 }
 # sources whose objects depend on the -D flags (the rest are built once and shared)
-FLAG_SOURCES = ("force.cu",)
+FLAG_SOURCES = ("force.cu", "search.cu")
 
 
 def build():
