@@ -13,7 +13,6 @@ OUT = os.path.join(ROOT, "scratch", "variants")
 VARIANTS = {
     "base": [],
     "rep0": ["-DNBX_PRUNE_REP=0"],  # prune: every active tile gets the full 32-pair test
-    "rep1m5": ["-DNBX_PRUNE_MINB=5"],  # row sweep at 5 CTAs/SM (no spills)
 }
 # sources whose objects depend on the -D flags (the rest are built once and shared)
 FLAG_SOURCES = ("force.cu", "search.cu")
