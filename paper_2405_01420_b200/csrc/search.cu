@@ -683,10 +683,14 @@ constexpr int PRUNE_JS = NBX_PRUNE_JS;
 struct PruneWarpSmem {
     float xj[3][32][PRUNE_JS];
     float4 xi[32];
+#if !NBX_PRUNE_REP
     unsigned pass[32]; // per pass: the hit ballot (4 lanes per item)
+#endif
     unsigned pidx[32];
     unsigned char item[256]; // entry << 3 | i-cluster
 #if NBX_PRUNE_REP
+    float4 xi1[8];            // row 1 of the 8 i clusters, contiguous: the row sweep's 8
+                              // distinct reads hit 8 bank quads (xi's 64-byte stride hits 2)
     unsigned char hit[256];   // per item: kept
     unsigned char item2[256]; // items the row sweep left open (indices into item)
 #endif
@@ -724,11 +728,16 @@ __device__ __forceinline__ float prune_r2min8(const float4& a, const float* xs, 
 }
 
 // one 4-lane-per-tile pass over items it (lane group g = lane / 4, row ii = lane % 4): hit of
-// this lane's row
+// this lane's row.  ROW1: the row sweep (ii == 1, from the contiguous row-1 copy)
+template <bool ROW1 = false>
 __device__ __forceinline__ bool prune_tile_rows(const PruneArgs& A, const PruneWarpSmem& S, unsigned it, int ii)
 {
     const int t = it >> 3, kk = it & 7;
+#if NBX_PRUNE_REP
+    const float4 a = ROW1 ? S.xi1[kk] : S.xi[4 * kk + ii];
+#else
     const float4 a = S.xi[4 * kk + ii];
+#endif
     const unsigned pidx = S.pidx[t];
     const float* xs = S.xj[0][t];
     const float* ys = S.xj[1][t];
@@ -752,7 +761,11 @@ __device__ __forceinline__ void prune_stage_i(const PruneArgs& A, const nbx_sci_
                se.cj_end <= A.n_cj);
     const float3 v = shift_vec(se.shift, A.box);
     const float4 t0 = A.xq_i[32 * se.sci + lane];
-    S.xi[lane] = make_float4(__fadd_rn(t0.x, v.x), __fadd_rn(t0.y, v.y), __fadd_rn(t0.z, v.z), 0.f);
+    const float4 a = make_float4(__fadd_rn(t0.x, v.x), __fadd_rn(t0.y, v.y), __fadd_rn(t0.z, v.z), 0.f);
+    S.xi[lane] = a;
+#if NBX_PRUNE_REP
+    if ((lane & 3) == 1) S.xi1[lane >> 2] = a;
+#endif
 }
 
 // one chunk of up to 32 cj entries starting at c0 of an entry ending at cj_end: returns this
@@ -807,7 +820,7 @@ __device__ __forceinline__ unsigned prune_chunk_packed(const PruneArgs& A, Prune
     for (int base = 0; base < total; base += 32) {
         const int m = base + lane;
         const unsigned it = m < total ? S.item[m] : 0u;
-        const bool h1 = prune_tile_rows(A, S, it, 1); // every lane: the test holds a warp vote
+        const bool h1 = prune_tile_rows<true>(A, S, it, 1); // every lane: the test holds a warp vote
         const bool hit = m < total && h1;
         if (m < total) S.hit[m] = hit ? 1 : 0;
         const unsigned open = __ballot_sync(full, m < total && !hit);
