@@ -802,6 +802,7 @@ __device__ __forceinline__ unsigned prune_chunk_packed(const PruneArgs& A, Prune
         if (lane >= d) incl += y;
     }
     const int total = __shfl_sync(full, incl, 31);
+    NBX_DCHECK(total <= 256); // 32 entries x 8 tiles: the item tables' size
     {
         unsigned mm = imask;
         int o = incl - pc;
