@@ -19,8 +19,9 @@
 // fill pass.
 //
 // Prune (default k_prune_packed): one warp per sci entry; per 32-entry chunk the active tiles
-// are compacted into an item table and tested 8 per warp pass (4 lanes per tile, packed
-// FP32x2 r^2 at rlist_inner); kept entries are compacted in order.  Short lists use the split
+// are compacted into an item table; a row sweep (one lane per tile, i atom 1 against the 8 j
+// atoms) keeps about half of them, and the rest are tested 8 per warp pass (4 lanes per tile,
+// packed FP32x2 r^2 at rlist_inner); kept entries are compacted in order.  Short lists use the split
 // form (a warp per chunk + a gather).  k_prune / k_prune_lanes / k_prune_fixed are opt-ins.
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
