@@ -12,8 +12,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "scratch", "variants")
 VARIANTS = {
     "base": [],
-    "noswz": ["-DNBX_PRUNE_SWZ=0"],  # prune: staged rows unswizzled
-    "rep0": ["-DNBX_PRUNE_REP=0"],  # prune: every active tile gets the full 32-pair test
+    "g2": ["-DNBX_VF_G=2"],  # energy kernels: the force's G(z) reciprocal without the Newton step
 }
 # sources whose objects depend on the -D flags (the rest are built once and shared)
 FLAG_SOURCES = ("force.cu", "search.cu")
