@@ -45,14 +45,18 @@ __global__ void k_get_f(int n, const int* __restrict__ islot, const float4* __re
 }
 
 // sum over real slots of x (x) f in fp64 -> acc[0..8]
+// sum over slots of (x - c) (x) f, c = the box centre: equal to sum x (x) f because the pair
+// forces sum to zero (Newton III), but the fp32 force roundings' net sum no longer enters
+// multiplied by the mean position (about half the error on a small box whose virial cancels
+// to ~1e-3 of sum |x (x) f|)
 __global__ void k_virial(int nslots, const int* __restrict__ order, const float4* __restrict__ xq,
-                         const float4* __restrict__ fc, double* acc)
+                         const float4* __restrict__ fc, double3 c, double* acc)
 {
     double w[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
     for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < nslots; s += gridDim.x * blockDim.x) {
         if (order[s] < 0) continue;
         float4 x = xq[s], f = fc[s];
-        double xv[3] = {x.x, x.y, x.z}, fv[3] = {f.x, f.y, f.z};
+        double xv[3] = {(double)x.x - c.x, (double)x.y - c.y, (double)x.z - c.z}, fv[3] = {f.x, f.y, f.z};
 #pragma unroll
         for (int a = 0; a < 3; a++)
 #pragma unroll
@@ -124,7 +128,8 @@ void virial_sum(nbx_ctx* ctx, int g, cudaStream_t st)
     if (!G.built || G.nslots == 0) return;
     int blocks = (G.nslots + 255) / 256;
     if (blocks > 4 * ctx->num_sms) blocks = 4 * ctx->num_sms;
-    k_virial<<<blocks, 256, 0, st>>>(G.nslots, G.order.p, G.xq.p, G.f.p, ctx->acc.p + 2 + 3 * NBX_NSHIFT);
+    const double3 c = make_double3(0.5 * ctx->box[0], 0.5 * ctx->box[1], 0.5 * ctx->box[2]);
+    k_virial<<<blocks, 256, 0, st>>>(G.nslots, G.order.p, G.xq.p, G.f.p, c, ctx->acc.p + 2 + 3 * NBX_NSHIFT);
     ctx->launches++;
     NBX_CUDA(cudaGetLastError());
 }
